@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the EvoX PSO/CSO generation on B200 (BASELINE.json metric).
+
+A "step" is one generation of the whole hot path (Philox r1/r2,
+velocity/position update + clip, fitness, pbest, gbest argmin, and for N>1
+the per-generation winner exchange) over the whole population.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config H|C1|C2|C3|C4g|C4r|C5]
+                    [--impl ours|reference] [--no-cpu-baseline]
+
+N>1 is launched with torchrun (one rank per GPU, NCCL): the population is
+row-sharded across ranks (strong scaling: fixed N_pop), one NCCL all-gather of
+the W winner records per generation.  Rank 0 prints ONE JSON line.
+
+--impl reference times the CPU oracle (the only reference this tier has) on a
+bounded row sample of the same workload, on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2301_12457_b200 import workloads as WL  # noqa: E402
+
+METRIC = "generations/s and individual-dims/s at 1/2/4/8 B200; % HBM roofline"
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            v = float(json.load(fh)["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs: copy, read+write bytes)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes(cfg, rows):
+    """Bytes one generation must move; DESIGN.md §5 states them.
+
+    PSO: per element X r+w (8), V r+w (8), P read-or-write (4) = 20 B; per row
+    imp r+w (2), pf read (4), f write (4) = 10 B (the rare pf write is not counted).
+    CSO: per loser element Xl r+w, Vl r+w, Xw read = 20 B, i.e. 10 B per population
+    element; per pair f reads (8) + loser f write (4) = 6 B per row."""
+    D = cfg.dim
+    if cfg.algo == "pso":
+        return 20 * D * rows + 10 * rows
+    return 10 * D * rows + 6 * rows
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.th is not None:
+            self.th.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v == "Active"})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "power_w_max": max(pw) if pw else None, "samples": len(self.rows)}
+
+
+def ncu_traffic(cfg_name):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        v = d.get(cfg_name, {}).get("dram_bytes_per_launch")
+        return float(v) if v is not None else None
+    except Exception:
+        return None
+
+
+def cpu_baseline(cfg, target_s=12.0):
+    """The oracle as it stands, on the host cores, over a bounded row sample of the workload
+    (2 generations: move + evaluate + tell), extrapolated to whole-population gens/s."""
+    import oracle as O
+    cores = os.cpu_count() or 1
+    lb, ub = WL.BOUNDS[cfg.problem]
+    D = cfg.dim
+    # ~54 ns per element per generation per core for PSO: size the sample
+    per_elem = 60e-9 / cores
+    rows = int(max(2, min(cfg.pop, target_s / 2 / (per_elem * D * (2 if cfg.algo == "pso" else 1)))))
+    t_gen = None
+    if cfg.algo == "pso":
+        st = O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=0, threads=cores)
+        t0 = time.perf_counter()
+        O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=2, state=st, threads=cores)
+        t_gen = (time.perf_counter() - t0) / 2
+    else:
+        B = max(2, rows // 8 if rows % 16 == 0 else rows)
+        X, V, f, F64 = O.cso_init(cfg.problem, rows, D, lb, ub, 0, threads=cores)
+        t0 = time.perf_counter()
+        for t in range(2):
+            O.cso_generation(cfg.problem, X, V, f, F64, B, t, 0, lb, ub, threads=cores)
+        t_gen = (time.perf_counter() - t0) / 2
+    frac = rows / cfg.pop
+    gens_per_s = frac / t_gen
+    return {"value": gens_per_s, "unit": "generations/s", "cores": cores, "kind": "oracle",
+            "sample": f"{rows} of {cfg.pop} rows x dim {D}, 2 generations (move+eval+tell), "
+                      f"{t_gen * 2:.2f} s; extrapolated linearly in rows",
+            "individual_dims_per_s": gens_per_s * cfg.pop * D * (0.5 if cfg.algo == "cso" else 1)}
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    import oracle as O
+    cores = os.cpu_count() or 1
+    lb, ub = WL.BOUNDS[cfg.problem]
+    D = cfg.dim
+    per_elem = 60e-9 / cores
+    budget = 150.0 / max(1, args.steps + args.warmup)  # whole run within a few minutes
+    rows = int(max(2, min(cfg.pop, budget / (per_elem * D * (2 if cfg.algo == "pso" else 1)))))
+    times = []
+    if cfg.algo == "pso":
+        st = O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=0, threads=cores)
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            st = O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=1, state=st, threads=cores)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    else:
+        B = max(2, rows // 8 if rows % 16 == 0 else rows)
+        X, V, f, F64 = O.cso_init(cfg.problem, rows, D, lb, ub, 0, threads=cores)
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.cso_generation(cfg.problem, X, V, f, F64, B, i, 0, lb, ub, threads=cores)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = (rows / cfg.pop) / t
+    sample = (f"{rows} of {cfg.pop} rows x dim {D} per step, oracle on {cores} host threads, "
+              f"extrapolated linearly in rows")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "generations/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3 * cfg.pop / rows, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.note, "algo": cfg.algo, "problem": cfg.problem,
+                       "pop": cfg.pop, "dim": cfg.dim},
+            "individual_dims_per_s": value * cfg.pop * D * (0.5 if cfg.algo == "cso" else 1),
+            "cpu_baseline": {"value": value, "unit": "generations/s", "cores": cores,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "generations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="H", choices=sorted(WL.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = WL.CONFIGS[args.config]
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_12457_b200 as ev
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nid = None
+    if world > 1:
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(ev.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        nid = bytes(buf.cpu().numpy().tobytes())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    lb, ub = WL.BOUNDS[cfg.problem]
+    Cls = ev.PSO if cfg.algo == "pso" else ev.CSO
+    kw = {} if cfg.algo == "pso" else {"block": cfg.pop // 8 if cfg.pop % 16 == 0 else 0}
+    h = Cls(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world, nccl_id=nid, **kw)
+    rows = h.info()["rows"]
+    stream = h.stream
+    h.step(cfg.problem, 0)          # generation 0: evaluate X0 + tell
+    h.step(cfg.problem, args.warmup)  # untimed warm-up generations (graph capture included)
+    h.sync()
+
+    # ---- timed region: K generations, device-timed with CUDA events on the handle's stream
+    h.set_timing(True)               # events around every generation kernel (dominant kernel)
+    h.kernel_time(reset=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h.step(cfg.problem, args.steps)
+    e1.record(stream)
+    h.sync()
+    barrier()
+    clk = clocks.stop()
+    ms_local = e0.elapsed_time(e1)
+    k_ms, k_n = h.kernel_time(reset=True)
+    h.set_timing(False)
+    t = torch.tensor([ms_local, k_ms / max(k_n, 1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, k_avg_ms = float(t[0]), float(t[1])
+    ms_per_step = ms_total / args.steps
+
+    # ---- end to end through the public API: step + D2H of the step's result, every step
+    import numpy as np
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        h.step(cfg.problem, 1)
+        best = h.best(with_row=True)  # synchronising D2H: fitness, index, best row
+    e2e_s = time.perf_counter() - t0
+    e2e = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e[0])
+
+    if rank == 0:
+        peak, peak_src = hbm_peak()
+        bytes_launch = algorithmic_bytes(cfg, rows)
+        achieved = bytes_launch / (k_avg_ms * 1e-3) / 1e9
+        traffic = ncu_traffic(args.config)
+        gens_per_s = 1e3 / ms_per_step
+        evaluated = cfg.pop * cfg.dim * (0.5 if cfg.algo == "cso" else 1.0)
+        line = {
+            "metric": METRIC,
+            "value": gens_per_s,
+            "unit": "generations/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.note, "algo": cfg.algo, "problem": cfg.problem,
+                       "pop": cfg.pop, "dim": cfg.dim, "seed": 0,
+                       "parallelism": f"row-sharded x{world}",
+                       "l2": "state (X,V,P) > L2: inputs larger than L2, no flush needed"
+                       if 12 * cfg.pop * cfg.dim > 2 * 126e6 else "state comparable to L2"},
+            "individual_dims_per_s": gens_per_s * evaluated,
+            "bytes_per_generation": algorithmic_bytes(cfg, cfg.pop),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": f"k_{cfg.algo}_gen<{cfg.problem}>",
+                         "kernel_ms": k_avg_ms, "bytes_per_launch": bytes_launch,
+                         "peak_source": peak_src},
+            "clocks": clk,
+            "gpu_launches": args.steps * (1 if (cfg.algo == "cso" or world == 1) else 2),
+            "e2e": {"value": args.e2e_steps / e2e_s, "unit": "generations/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 + 8 + 4 * cfg.dim,
+                    "note": "per step: evox_*_step(1) through the C-ABI + synchronising "
+                            "best() D2H (fitness, index, best row) into host memory"},
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

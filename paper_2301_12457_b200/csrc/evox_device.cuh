@@ -1,0 +1,181 @@
+// evox_device.cuh -- device building blocks of the B200 PSO/CSO generation.
+//
+// Written independently of oracle/ (no shared code); both follow PAPER.md /
+// SPEC.md and the readings R-1..R-13 of DESIGN.md §3.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace evox {
+
+enum Problem : int { SPHERE = 0, ACKLEY = 1, RASTRIGIN = 2, GRIEWANK = 3, ROSENBROCK = 4 };
+
+// ------------------------------------------------------------------ Philox
+// Philox4x32-10 (Salmon et al., SC'11): R-6.  The multiplies compile to
+// IMAD.WIDE.U32 (hi and lo in one instruction); the three-input XORs to LOP3.
+// The key schedule k + r*W is uniform across the grid.
+struct Philox {
+    static constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    static constexpr uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+    __device__ __forceinline__ static uint4 run(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            const uint64_t p0 = (uint64_t)M0 * c.x;
+            const uint64_t p1 = (uint64_t)M1 * c.z;
+            const uint32_t rk0 = k0 + (uint32_t)r * W0, rk1 = k1 + (uint32_t)r * W1;
+            uint4 n;
+            n.x = (uint32_t)(p1 >> 32) ^ c.y ^ rk0;
+            n.y = (uint32_t)p1;
+            n.z = (uint32_t)(p0 >> 32) ^ c.w ^ rk1;
+            n.w = (uint32_t)p0;
+            c = n;
+        }
+        return c;
+    }
+};
+
+// 24-bit uniform in [0,1): (b >> 8) * 2^-24 (exact).  R-6.
+__device__ __forceinline__ float u24(uint32_t b) {
+    return __fmul_rn(__uint2float_rn(b >> 8), 0x1p-24f);
+}
+
+// -------------------------------------------------------- argmin keys (R-5)
+// Order-preserving f32 -> u32 (NaN -> +inf, -0 -> +0); key = ord << 32 | row.
+__device__ __forceinline__ uint32_t ord_f32(float f) {
+    if (f != f) f = __int_as_float(0x7f800000);
+    if (f == 0.0f) f = 0.0f;
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(uint32_t o) {
+    const uint32_t b = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+    return __uint_as_float(b);
+}
+__device__ __forceinline__ unsigned long long make_key(float f, long long global_row) {
+    return ((unsigned long long)ord_f32(f) << 32) | (unsigned long long)(uint32_t)global_row;
+}
+
+// ------------------------------------------------------------ memory hints
+// Streaming (evict-first) loads/stores for the population: each element is
+// touched once per generation and the state (12 GB at the headline config)
+// is far larger than L2, so keep L2 for G, bounds, f/pf/imp.
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
+
+// --------------------------------------------------------- fitness (R-7)
+// fp32 forms that are algebraically identical to the textbook definitions
+// but free of cancellation near the optimum:
+//   Ackley:    -20 expm1(-0.2 sqrt(S2/D)) - e expm1(-2 SS/D), SS = sum sin^2(pi x)
+//              (sum cos(2 pi x) = D - 2 SS)
+//   Rastrigin: sum (x^2 + 20 sin^2(pi x))           (10 - 10 cos 2 pi x = 20 sin^2 pi x)
+//   Griewank:  S2/4000 + q, q = 1 - prod cos(x_j h_j) accumulated as the complement
+//              product q <- q + a - q a, a_j = 2 sin^2(x_j h_j / 2), h_j = 1/sqrt(j+1)
+//   Rosenbrock: sum 100 d^2 + (1-x_j)^2, d = fmaf(-x_j, x_j, x_{j+1})
+// Per-lane sequential accumulation, then a fixed xor-shuffle tree and a fixed
+// cross-warp order: the reduction order depends on dim only, never on the
+// shard, grid or population size (=> bitwise identical across W, R-11).
+template <int P> struct Fit;
+
+__device__ __forceinline__ float sin2pi(float x) {  // sin^2(pi x)
+    const float s = sinpif(x);
+    return __fmul_rn(s, s);
+}
+
+template <> struct Fit<SPHERE> {
+    float s = 0.0f;
+    __device__ __forceinline__ void elem(float x, int64_t) { s = __fmaf_rn(x, x, s); }
+    __device__ __forceinline__ void combine(const Fit& o) { s = __fadd_rn(s, o.s); }
+    __device__ __forceinline__ void shfl_xor(int m) { s = __shfl_xor_sync(0xffffffffu, s, m); }
+    __device__ __forceinline__ float finish(int64_t) const { return s; }
+};
+
+template <> struct Fit<ACKLEY> {
+    float s2 = 0.0f, ss = 0.0f;
+    __device__ __forceinline__ void elem(float x, int64_t) {
+        s2 = __fmaf_rn(x, x, s2);
+        ss = __fadd_rn(ss, sin2pi(x));
+    }
+    __device__ __forceinline__ void combine(const Fit& o) {
+        s2 = __fadd_rn(s2, o.s2);
+        ss = __fadd_rn(ss, o.ss);
+    }
+    __device__ __forceinline__ void shfl_xor(int m) {
+        s2 = __shfl_xor_sync(0xffffffffu, s2, m);
+        ss = __shfl_xor_sync(0xffffffffu, ss, m);
+    }
+    __device__ __forceinline__ float finish(int64_t D) const {
+        const float invD = __frcp_rn((float)D);
+        const float a = -20.0f * expm1f(-0.2f * sqrtf(__fmul_rn(s2, invD)));
+        const float b = -2.718281828459045f * expm1f(-2.0f * __fmul_rn(ss, invD));
+        return __fadd_rn(a, b);
+    }
+};
+
+template <> struct Fit<RASTRIGIN> {
+    float s = 0.0f;
+    __device__ __forceinline__ void elem(float x, int64_t) {
+        s = __fadd_rn(s, __fmaf_rn(20.0f, sin2pi(x), __fmul_rn(x, x)));
+    }
+    __device__ __forceinline__ void combine(const Fit& o) { s = __fadd_rn(s, o.s); }
+    __device__ __forceinline__ void shfl_xor(int m) { s = __shfl_xor_sync(0xffffffffu, s, m); }
+    __device__ __forceinline__ float finish(int64_t) const { return s; }
+};
+
+template <> struct Fit<GRIEWANK> {
+    float s2 = 0.0f, q = 0.0f;
+    __device__ __forceinline__ void elem(float x, int64_t j) {
+        s2 = __fmaf_rn(x, x, s2);
+        const float h = __fmul_rn(0.5f, __frsqrt_rn((float)(j + 1)));  // 1/(2 sqrt(j+1))
+        const float sn = sinf(__fmul_rn(x, h));
+        const float a = __fmul_rn(2.0f, __fmul_rn(sn, sn));  // 1 - cos(x/sqrt(j+1))
+        q = __fmaf_rn(-q, a, __fadd_rn(q, a));
+    }
+    __device__ __forceinline__ void combine(const Fit& o) {
+        s2 = __fadd_rn(s2, o.s2);
+        q = __fmaf_rn(-q, o.q, __fadd_rn(q, o.q));
+    }
+    __device__ __forceinline__ void shfl_xor(int m) {
+        s2 = __shfl_xor_sync(0xffffffffu, s2, m);
+        q = __shfl_xor_sync(0xffffffffu, q, m);
+    }
+    __device__ __forceinline__ float finish(int64_t) const {
+        return __fadd_rn(__fmul_rn(s2, 1.0f / 4000.0f), q);
+    }
+};
+
+template <> struct Fit<ROSENBROCK> {
+    float s = 0.0f;
+    __device__ __forceinline__ void elem(float, int64_t) {}
+    __device__ __forceinline__ void pair(float x, float xn) {  // term j with x_j, x_{j+1}
+        const float d = __fmaf_rn(-x, x, xn);
+        const float e = __fsub_rn(1.0f, x);
+        s = __fadd_rn(s, __fmaf_rn(__fmul_rn(100.0f, d), d, __fmul_rn(e, e)));
+    }
+    __device__ __forceinline__ void combine(const Fit& o) { s = __fadd_rn(s, o.s); }
+    __device__ __forceinline__ void shfl_xor(int m) { s = __shfl_xor_sync(0xffffffffu, s, m); }
+    __device__ __forceinline__ float finish(int64_t) const { return s; }
+};
+
+// Sphere/Ackley/Rastrigin/Griewank fold all valid lanes of a quad; Rosenbrock
+// folds the three intra-quad pairs (the pair crossing into the next quad is
+// handled by the row engine with a shuffle / carried value).
+template <int P>
+__device__ __forceinline__ void fit_quad(Fit<P>& acc, float4 x, int64_t j0, int64_t D) {
+    if (j0 + 3 < D) {
+        acc.elem(x.x, j0); acc.elem(x.y, j0 + 1); acc.elem(x.z, j0 + 2); acc.elem(x.w, j0 + 3);
+    } else {
+        if (j0 < D) acc.elem(x.x, j0);
+        if (j0 + 1 < D) acc.elem(x.y, j0 + 1);
+        if (j0 + 2 < D) acc.elem(x.z, j0 + 2);
+    }
+}
+template <>
+__device__ __forceinline__ void fit_quad<ROSENBROCK>(Fit<ROSENBROCK>& acc, float4 x, int64_t j0,
+                                                     int64_t D) {
+    if (j0 + 1 < D) acc.pair(x.x, x.y);
+    if (j0 + 2 < D) acc.pair(x.y, x.z);
+    if (j0 + 3 < D) acc.pair(x.z, x.w);
+}
+
+}  // namespace evox

@@ -1,0 +1,96 @@
+// evox_internal.h -- structures shared by the kernel TU and the C-ABI TU.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace evox {
+
+// Device-resident control block of a handle.  Kernels read the generation
+// index from here (not from launch parameters) so one captured CUDA graph can
+// be replayed for any generation.
+struct Ctl {
+    unsigned long long gen_key;  // atomicMin accumulator of the running generation (~0 at rest)
+    unsigned int ticket;         // CTAs finished in the running kernel (0 at rest)
+    unsigned int phase;          // unused by kernels
+    unsigned long long t;        // index of the current population
+    float gf;                    // best-so-far fitness (PSO) / scratch
+    int pad;
+    long long gidx;              // global row of gbest (-1: none)
+    float* hist;                 // hist[t] = min f of generation t
+    unsigned long long* hkeys;   // CSO, world > 1: per-generation local min keys
+    unsigned long long hist_cap;
+};
+
+// One rank's PSO state, as seen by kernels.
+struct PsoArgs {
+    float* X;
+    float* V;
+    float* P;
+    float* f;
+    float* pf;
+    unsigned char* imp;  // pending pbest copy (lazy pbest)
+    float* G;            // gbest row [ld]
+    const float* lb;     // [ld] (used when !uniform_bounds)
+    const float* ub;
+    float lb0, ub0;
+    int uniform_bounds;
+    long long rows, row0, D, ld;
+    float w, phi_p, phi_g;
+    unsigned int k0, k1;  // Philox key = seed
+    Ctl* ctl;
+    unsigned char* rec;   // world > 1: W winner records, stride rec_stride bytes
+    long long rec_stride;
+    int rank, world;
+    int exchange;  // 1: publish the local winner record for the NCCL exchange (A13)
+};
+
+struct CsoArgs {
+    float* X;
+    float* V;
+    float* f;
+    const float* lb;
+    const float* ub;
+    float lb0, ub0;
+    int uniform_bounds;
+    long long rows, row0, D, ld, pop;
+    long long B;  // pairing block size
+    float phi;
+    const float* xbar;  // [ld] column means (phi != 0)
+    unsigned int k0, k1;
+    Ctl* ctl;
+    int rank, world;
+    int exchange;  // 1: per-generation keys go to hkeys for one NCCL min-reduction per call
+};
+
+// Launch configuration is a function of dim only (R-11: bitwise identical
+// results for every shard count and population size).
+int wpr_for_dim(long long ld);
+
+// ---- launchers (evox_kernels.cu); all asynchronous on `st`.
+cudaError_t launch_pso_init(const PsoArgs& a, cudaStream_t st);
+cudaError_t launch_eval(int problem, const float* X, long long rows, long long D, long long ld,
+                        float* fit, cudaStream_t st);
+cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_pso_move(const PsoArgs& a, unsigned long long t, cudaStream_t st);
+cudaError_t launch_pso_tell(const PsoArgs& a, const float* fit, unsigned long long t,
+                            cudaStream_t st);
+cudaError_t launch_gbest_select(const PsoArgs& a, cudaStream_t st);
+cudaError_t launch_pso_materialize(const PsoArgs& a, cudaStream_t st);
+int pso_gen_grid(int problem, long long ld, long long rows, int device);
+
+cudaError_t launch_cso_init(const CsoArgs& a, cudaStream_t st);
+cudaError_t launch_cso_tell0(const CsoArgs& a, cudaStream_t st);
+int cso_gen_grid(int problem, const CsoArgs& a, int device);
+cudaError_t launch_cso_gen(int problem, const CsoArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_cso_colmean(const CsoArgs& a, float* xbar, double* scratch, cudaStream_t st);
+cudaError_t launch_cso_hist_from_keys(const CsoArgs& a, unsigned long long t0, long long n,
+                                      cudaStream_t st);
+cudaError_t launch_argmin_rows(const float* f, long long rows, long long row0,
+                               unsigned long long* key_out, cudaStream_t st);
+
+cudaError_t launch_debug_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
+                                long long n, cudaStream_t st);
+
+}  // namespace evox

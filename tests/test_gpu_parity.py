@@ -1,0 +1,435 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bars (R-9): Philox words and X0 bit-exact; fitness within
+max(1e-5 |F64|, 1e-6); positions within 1e-6 relative (observed bit-exact);
+pbest/gbest decisions exact outside near-ties, near-ties re-synchronised and
+logged; checkpoints at 1, 10 and 100 generations.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from parity import (assert_fitness, assert_positions, compare_pso, gpu_pso_state,
+                    resync_oracle_from_gpu)
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2301_12457_b200 as ev  # noqa: E402
+from paper_2301_12457_b200 import evox as E  # noqa: E402
+from paper_2301_12457_b200 import workloads as WL  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    torch.cuda.set_device(0)
+
+
+# ------------------------------------------------------------------ Philox
+def test_philox_gpu_matches_kat_and_oracle(golden_dir):
+    import os
+    kat = []
+    for line in open(os.path.join(golden_dir, "philox_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        v = [int(x, 16) for x in line.split()]
+        kat.append(v)
+    for v in kat:
+        ctr = torch.tensor(np.array([v[0:4]], np.uint32).view(np.int32), device="cuda")
+        out = E.debug_philox(ctr, v[4], v[5]).cpu().numpy().view(np.uint32)[0]
+        assert list(out) == v[6:10]
+    rng = np.random.default_rng(0)
+    C = rng.integers(0, 2 ** 32, (4096, 4), dtype=np.uint64).astype(np.uint32)
+    key = (0xDEADBEEF, 0x12345678)
+    out = E.debug_philox(torch.tensor(C.view(np.int32), device="cuda"), *key).cpu().numpy()
+    out = out.view(np.uint32)
+    for i in range(0, 4096, 97):
+        assert list(out[i]) == list(O.philox(C[i], key))
+
+
+# -------------------------------------------------------------------- init
+@pytest.mark.parametrize("N,D", [(1, 1), (7, 3), (100, 10), (33, 37), (64, 1000), (5, 4099),
+                                 (3, 40001)])
+def test_init_bitwise(N, D):
+    lb = np.linspace(-3, -1, D).astype(np.float32)
+    ub = np.linspace(1, 600, D).astype(np.float32)
+    pso = ev.PSO(N, D, lb, ub, seed=1234567890123)
+    X = pso.view("X").cpu().numpy()
+    V = pso.view("V").cpu().numpy()
+    Xo, Vo = O.pso_init(N, D, 0, lb, ub, 1234567890123)
+    assert np.array_equal(X[:, :D], Xo)
+    assert not X[:, D:].any() and not V.any()
+    assert np.array_equal(pso.view("P").cpu().numpy(), X)
+
+
+# -------------------------------------------------------------------- eval
+EVAL_SHAPES = [(1, 1), (3, 2), (5, 3), (64, 4), (100, 10), (37, 33), (513, 1000), (16, 1001),
+               (8, 4099), (3, 40001), (2, 100000)]
+
+
+@pytest.mark.parametrize("problem", list(WL.BOUNDS))
+@pytest.mark.parametrize("N,D", EVAL_SHAPES)
+def test_eval_parity(problem, N, D):
+    for k, X in enumerate((WL.uniform_rows(N, D, problem, seed=D + N),
+                           WL.uniform_rows(N, D, problem, seed=7, scale=1e-2),
+                           WL.near_optimum_rows(N, D, problem, seed=3, radius=1e-4))):
+        Xp = torch.from_numpy(WL.padded(X)).cuda()
+        f = ev.evaluate(problem, Xp, dim=D).cpu().numpy()
+        assert_fitness(f, O.evaluate(problem, X), f"{problem} {N}x{D} input {k}")
+
+
+def test_eval_closed_forms_gpu():
+    D = 1003
+    z = np.zeros((1, D), np.float32)
+    for p in WL.BOUNDS:
+        x = z if p != "rosenbrock" else z + 1
+        f = ev.evaluate(p, torch.from_numpy(WL.padded(x)).cuda(), dim=D).item()
+        assert abs(f) <= 1e-6, (p, f)
+    k = np.random.default_rng(1).integers(-5, 6, (4, D)).astype(np.float32)
+    f = ev.evaluate("rastrigin", torch.from_numpy(WL.padded(k)).cuda(), dim=D).cpu().numpy()
+    assert np.array_equal(f, (k.astype(np.float64) ** 2).sum(1).astype(np.float32))
+    f = ev.evaluate("rosenbrock", torch.from_numpy(WL.padded(z)).cuda(), dim=D).item()
+    assert f == D - 1
+
+
+def test_eval_permutation_and_empty():
+    X = WL.uniform_rows(300, 57, "griewank", 5)
+    perm = np.random.default_rng(2).permutation(300)
+    a = ev.evaluate("griewank", torch.from_numpy(WL.padded(X)).cuda(), dim=57).cpu().numpy()
+    b = ev.evaluate("griewank", torch.from_numpy(WL.padded(X[perm])).cuda(), dim=57).cpu().numpy()
+    assert np.array_equal(a[perm], b)
+    e = ev.evaluate("sphere", torch.zeros((0, 8), device="cuda"), dim=5)
+    assert e.numel() == 0
+
+
+# ----------------------------------------------------------------- PSO step
+PSO_CASES = [("sphere", 100, 10, -5.12, 5.12, 0),        # C1
+             ("ackley", 64, 37, -32.768, 32.768, 1),
+             ("rastrigin", 50, 8, -5.12, 5.12, 2),
+             ("griewank", 40, 100, -600, 600, 3),
+             ("rosenbrock", 33, 101, -5, 10, 4),
+             ("rosenbrock", 9, 4099, -5, 10, 5),
+             ("ackley", 6, 40001, -32.768, 32.768, 6)]
+
+
+def _run_parity(problem, N, D, lb, ub, seed, gens, checkpoints=(1, 10, 100)):
+    pso = ev.PSO(N, D, lb, ub, seed=seed)
+    pso.step(problem, 0)
+    st = O.pso_run(problem, N, D, lb, ub, seed=seed, n_gens=0)
+    g = gpu_pso_state(pso, D)
+    flips = compare_pso(g, st, label=f"{problem} t=0")
+    if flips:
+        st = resync_oracle_from_gpu(st, g)
+    log = []
+    for t in range(1, gens + 1):
+        prev_pf = g["pf"]
+        pso.step(problem, 1)
+        st = O.pso_run(problem, N, D, lb, ub, seed=seed, n_gens=1, state=st)
+        g = gpu_pso_state(pso, D)
+        flips = compare_pso(g, st, prev_pf_gpu=prev_pf, label=f"{problem} t={t}")
+        if flips:
+            log.append((t, flips))
+            st = resync_oracle_from_gpu(st, g)
+        if t in checkpoints:
+            # full-state checkpoint (R-9): X, V, P, pf, f, G, gf
+            assert_positions(g["X"], st.X, f"checkpoint {t} X")
+            assert_positions(g["P"], st.P, f"checkpoint {t} P")
+            assert_positions(g["G"], st.G, f"checkpoint {t} G")
+            assert_fitness(g["f"], st.F64, f"checkpoint {t} f")
+    return pso, log
+
+
+@pytest.mark.parametrize("problem,N,D,lb,ub,seed", PSO_CASES)
+def test_pso_step_parity_100_gens(problem, N, D, lb, ub, seed):
+    gens = 100 if D <= 1000 else 10
+    pso, log = _run_parity(problem, N, D, lb, ub, seed, gens)
+    if log:
+        print(f"near-tie resyncs ({problem}): {log}")
+    assert len(log) <= gens // 10, log  # near-ties are rare
+
+
+@pytest.mark.parametrize("problem,N,D,lb,ub,seed", PSO_CASES[:5])
+def test_pso_graphed_equals_stepwise(problem, N, D, lb, ub, seed):
+    """step(100) in one call (CUDA-graph replay) is bitwise equal to 100 x step(1)."""
+    a = ev.PSO(N, D, lb, ub, seed=seed)
+    a.step(problem, 100)
+    b = ev.PSO(N, D, lb, ub, seed=seed)
+    b.step(problem, 0)
+    for _ in range(100):
+        b.step(problem, 1)
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
+        assert np.array_equal(ga[k], gb[k]), k
+    assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
+
+
+def test_pso_c1_oneshot_matches_oracle():
+    """C1 (PSO/Sphere 100x10, 100 generations, seed 0) in one step(100) call."""
+    pso = ev.PSO(100, 10, -5.12, 5.12, seed=0)
+    pso.step("sphere", 100)
+    st = O.pso_run("sphere", 100, 10, -5.12, 5.12, seed=0, n_gens=100)
+    g = gpu_pso_state(pso, 10)
+    assert_positions(g["X"], st.X, "C1 X")
+    assert_fitness(g["hist"], np.asarray(st.hist, np.float64), "C1 hist")
+    assert g["gidx"] == st.gidx
+    assert g["gf"] < 1e-4  # S:321-style convergence on the GPU as well
+
+
+def test_pso_ask_tell_equals_step():
+    """Unfused ask/evaluate/tell produces the same state as fused step (bitwise)."""
+    N, D, p = 70, 45, "ackley"
+    a = ev.PSO(N, D, -32.768, 32.768, seed=11)
+    a.step(p, 12)
+    b = ev.PSO(N, D, -32.768, 32.768, seed=11)
+    for _ in range(13):
+        X = b.ask()
+        f = ev.evaluate(p, X, dim=D, stream=b.stream)
+        b.tell(f)
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
+        assert np.array_equal(ga[k], gb[k]), k
+
+
+def test_pso_ask_tell_external_fitness_vs_oracle():
+    """tell() with caller fitness (here: a shifted Sphere computed by torch) follows the
+    oracle's tell/move primitives."""
+    N, D, seed = 40, 12, 5
+    pso = ev.PSO(N, D, -2, 2, seed=seed)
+    X, V = O.pso_init(N, D, 0, -2, 2, seed)
+    P, pf = X.copy(), np.full(N, np.inf, np.float32)
+    G, gf = np.zeros(D, np.float32), np.inf
+    for t in range(6):
+        Xg = pso.ask()
+        assert np.array_equal(Xg.cpu().numpy()[:, :D], X), t
+        fx = ((Xg[:, :D] - 0.25) ** 2).sum(1).contiguous()
+        pso.tell(fx)
+        f = fx.cpu().numpy()
+        O.pso_tell_rows(X, f, P, pf)
+        i, m = O.argmin(f)
+        if m < gf:
+            gf, G = m, X[i].copy()
+        O.pso_move(X, V, P, G, 0, t, seed, 0.6, 2.5, 0.8, -2, 2)
+    b = pso.best()
+    assert b[0] == gf and np.array_equal(b[2], G)
+
+
+def test_pso_contract_errors():
+    pso = ev.PSO(16, 8, -1, 1, seed=0)
+    with pytest.raises(E.ContractError):
+        pso.tell(torch.zeros(16, device="cuda"))
+    pso.ask()
+    with pytest.raises(E.ContractError):
+        pso.ask()
+    with pytest.raises(E.ContractError):
+        pso.step("sphere", 1)
+    pso.tell(torch.zeros(16, device="cuda"))
+    pso.step("sphere", 2)
+    with pytest.raises(E.ContractError):
+        pso.step("ackley", 1)
+    with pytest.raises(E.InvalidArgument):
+        pso.step("sphere", -1)
+
+
+def test_pso_save_load_roundtrip():
+    N, D, p = 64, 33, "rastrigin"
+    a = ev.PSO(N, D, -5.12, 5.12, seed=9)
+    a.step(p, 5)
+    blob = a.save()
+    a.step(p, 7)
+    b = ev.PSO(N, D, -5.12, 5.12, seed=9)
+    b.load(blob)
+    b.step(p, 7)
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
+        assert np.array_equal(ga[k], gb[k]), k
+    c = ev.PSO(N, D, -5.12, 5.12, seed=10)
+    with pytest.raises(E.ContractError):
+        c.load(blob)
+
+
+def test_pso_view_p_materialise_is_neutral():
+    """Reading P (materialising lazy pbest rows) does not change later generations."""
+    N, D, p = 48, 20, "griewank"
+    a = ev.PSO(N, D, -600, 600, seed=4)
+    b = ev.PSO(N, D, -600, 600, seed=4)
+    for _ in range(8):
+        a.step(p, 1)
+        b.step(p, 1)
+        b.view("P")
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G"):
+        assert np.array_equal(ga[k], gb[k]), k
+
+
+def test_pso_user_stream_and_workspace():
+    N, D, p = 128, 64, "sphere"
+    s = torch.cuda.Stream()
+    ws = torch.empty(ev.PSO.workspace_bytes(N, D), dtype=torch.uint8, device="cuda")
+    a = ev.PSO(N, D, -5.12, 5.12, seed=3, stream=s, workspace=ws)
+    a.step(p, 10)
+    b = ev.PSO(N, D, -5.12, 5.12, seed=3)
+    b.step(p, 10)
+    assert np.array_equal(gpu_pso_state(a, D)["X"], gpu_pso_state(b, D)["X"])
+    assert a.info()["stream"] == s.cuda_stream
+
+
+def test_pso_nccl_exchange_path_single_rank(monkeypatch):
+    """EVOX_FORCE_NCCL=1: the multi-GPU exchange (record all-gather + gbest select) on a
+    1-rank communicator gives the same trajectory bitwise as the direct path."""
+    N, D, p = 96, 50, "ackley"
+    a = ev.PSO(N, D, -32.768, 32.768, seed=21)
+    a.step(p, 15)
+    monkeypatch.setenv("EVOX_FORCE_NCCL", "1")
+    b = ev.PSO(N, D, -32.768, 32.768, seed=21)
+    b.step(p, 15)
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
+        assert np.array_equal(ga[k], gb[k]), k
+    assert ga["gidx"] == gb["gidx"]
+
+
+# ---------------------------------------------------- full-size sampled checks
+def _sampled_generation_check(problem, N, D, seed, n_sample=64):
+    """At full size: run generation 0 (+ one move) on the GPU, recompute sampled rows
+    one by one with the oracle from the GPU's pre-move state, and check argmin
+    properties on the whole population."""
+    lb, ub = WL.BOUNDS[problem]
+    pso = ev.PSO(N, D, lb, ub, seed=seed)
+    pso.step(problem, 0)
+    rng = np.random.default_rng(seed)
+    rows = np.unique(np.concatenate([[0, N - 1], rng.integers(0, N, n_sample)]))
+    Xv = pso.view("X")
+    X0 = Xv[rows].cpu().numpy()[:, :D].copy()
+    V0 = pso.view("V")[rows].cpu().numpy()[:, :D].copy()
+    P0 = pso.view("P")[rows].cpu().numpy()[:, :D].copy()
+    G0 = pso.view("G").cpu().numpy()[:D].copy()
+    f0 = pso.view("F").cpu().numpy()
+    # generation 0 properties: the argmin over the whole population
+    gf, gi, grow = pso.best()
+    m = f0.min()
+    assert gf == m and gi == int(np.nonzero(f0 == m)[0][0])
+    assert np.array_equal(grow, pso.view("X")[gi].cpu().numpy()[:D])
+    assert_fitness(f0[rows], O.evaluate(problem, X0), "gen0 sampled f")
+    pso.step(problem, 1)
+    X1 = pso.view("X")[rows].cpu().numpy()[:, :D]
+    V1 = pso.view("V")[rows].cpu().numpy()[:, :D]
+    f1 = pso.view("F").cpu().numpy()
+    for k, r in enumerate(rows):
+        x, v = X0[k:k + 1].copy(), V0[k:k + 1].copy()
+        O.pso_move(x, v, P0[k:k + 1], G0, int(r), 0, seed, WL.W, WL.PHI_P, WL.PHI_G, lb, ub)
+        assert np.array_equal(X1[k], x[0]), f"row {r} X"
+        assert np.array_equal(V1[k], v[0]), f"row {r} V"
+    assert_fitness(f1[rows], O.evaluate(problem, X1), "gen1 sampled f")
+    gf1, gi1, _ = pso.best(with_row=False)
+    assert gf1 == min(gf, f1.min())
+    h = pso.history()
+    assert len(h) == 2 and h[0] == f0.min() and h[1] == f1.min()
+    pso.close()
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C4g", "C4r", "C5", "H"])
+def test_full_size_sampled(cfg):
+    c = WL.CONFIGS[cfg]
+    free, _ = torch.cuda.mem_get_info()
+    need = 3 * c.pop * WL.round4(c.dim) * 4 * 1.1
+    if need > free:
+        pytest.skip("not enough device memory")
+    _sampled_generation_check(c.problem, c.pop, c.dim, seed=0)
+
+
+def test_c2_full_parity_10_gens():
+    """C2 (PSO/Ackley 1e4 x 1000) compared element by element for 10 generations."""
+    c = WL.CONFIGS["C2"]
+    lb, ub = WL.BOUNDS[c.problem]
+    pso = ev.PSO(c.pop, c.dim, lb, ub, seed=0)
+    pso.step(c.problem, 10)
+    st = O.pso_run(c.problem, c.pop, c.dim, lb, ub, seed=0, n_gens=10, threads=8)
+    g = gpu_pso_state(pso, c.dim)
+    flips = compare_pso(g, st, label="C2 t=10")
+    assert not flips, flips
+
+
+# ------------------------------------------------------------------- CSO
+def _cso_parity(problem, N, D, B, seed, gens, phi=0.0):
+    lb, ub = WL.BOUNDS[problem]
+    cso = ev.CSO(N, D, lb, ub, phi=phi, block=B, seed=seed)
+    cso.step(problem, 0)
+    X, V, f, F64 = O.cso_init(problem, N, D, lb, ub, seed)
+    hist = [float(f.min())]
+    resync = 0
+    for t in range(gens):
+        cso.step(problem, 1)
+        O.cso_generation(problem, X, V, f, F64, B, t, seed, lb, ub, phi=phi)
+        hist.append(float(f.min()))
+        Xg = cso.view("X").cpu().numpy()[:, :D]
+        Vg = cso.view("V").cpu().numpy()[:, :D]
+        fg = cso.view("F").cpu().numpy()
+        if not np.array_equal(Xg, X):
+            # a flipped winner at a near-tie: adopt the GPU state (R-9) -- must be rare
+            resync += 1
+            X, V, f = Xg.copy(), Vg.copy(), fg.copy()
+            F64 = O.evaluate(problem, X)
+            continue
+        assert np.array_equal(Vg, V)
+        assert_fitness(fg, O.evaluate(problem, Xg), f"CSO t={t + 1} f")
+        f = fg.copy()  # decisions use the GPU's fp32 fitness from here on
+    h = cso.history()
+    assert len(h) == gens + 1
+    assert (np.diff(h) <= 0).all()  # min f is non-increasing (winners are kept)
+    return resync
+
+
+@pytest.mark.parametrize("problem,N,D,B", [("rastrigin", 64, 33, 8), ("sphere", 100, 10, 100),
+                                           ("ackley", 50, 100, 16), ("griewank", 33, 7, 33),
+                                           ("rosenbrock", 40, 4099, 10)])
+def test_cso_parity(problem, N, D, B):
+    resync = _cso_parity(problem, N, D, B, seed=3, gens=20 if D < 1000 else 4)
+    assert resync <= 2
+
+
+def test_cso_phi_nonzero_parity():
+    assert _cso_parity("sphere", 64, 20, 16, seed=5, gens=10, phi=0.1) <= 1
+
+
+def test_cso_nccl_path_single_rank(monkeypatch):
+    N, D, p = 128, 40, "rastrigin"
+    a = ev.CSO(N, D, -5.12, 5.12, block=16, seed=8)
+    a.step(p, 12)
+    monkeypatch.setenv("EVOX_FORCE_NCCL", "1")
+    b = ev.CSO(N, D, -5.12, 5.12, block=16, seed=8)
+    b.step(p, 12)
+    assert np.array_equal(a.view("X").cpu().numpy(), b.view("X").cpu().numpy())
+    assert np.array_equal(a.history(), b.history())
+    assert a.best()[:2] == b.best()[:2]
+
+
+def test_cso_c3_sampled():
+    """C3 (CSO/Rastrigin 1e5 x 1000): one generation, sampled pairs recomputed by the oracle."""
+    c = WL.CONFIGS["C3"]
+    lb, ub = WL.BOUNDS[c.problem]
+    B = c.pop // 8
+    cso = ev.CSO(c.pop, c.dim, lb, ub, block=B, seed=0)
+    cso.step(c.problem, 0)
+    X0 = cso.view("X").cpu().numpy()[:, :c.dim].copy()
+    f0 = cso.view("F").cpu().numpy().copy()
+    cso.step(c.problem, 1)
+    X1 = cso.view("X").cpu().numpy()[:, :c.dim]
+    V1 = cso.view("V").cpu().numpy()[:, :c.dim]
+    f1 = cso.view("F").cpu().numpy()
+    changed = (X1 != X0).any(1)
+    assert changed.sum() <= c.pop // 2
+    rng = np.random.default_rng(0)
+    for blk in (0, 7):
+        pairs = O.cso_pairs(B, blk, 0, 0)
+        for a, b in pairs[rng.integers(0, len(pairs), 8)]:
+            i, k = blk * B + a, blk * B + b
+            w, l = (i, k) if (f0[i] < f0[k] or (f0[i] == f0[k] and i < k)) else (k, i)
+            assert np.array_equal(X1[w], X0[w])
+            xl, vl = X0[l].copy(), np.zeros(c.dim, np.float32)
+            R1 = O.draw(1, c.dim, l, 0, 5, 0)[0]
+            R2 = O.draw(1, c.dim, l, 0, 6, 0)[0]
+            O.cso_loser_update_with(X0[w], xl, vl, R1, R2, lb=lb, ub=ub)
+            assert np.array_equal(X1[l], xl) and np.array_equal(V1[l], vl)
+    assert_fitness(f1[changed][:256], O.evaluate(c.problem, X1[changed][:256]), "C3 f")
