@@ -212,9 +212,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--pop", type=int, default=0, help="override the population (profiling only)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = WL.CONFIGS[args.config]
+    if args.pop:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, pop=args.pop, note=cfg.note + f" [pop override {args.pop}]")
 
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)

@@ -32,7 +32,8 @@ def _newest_input() -> float:
 
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
-    cmd = [NVCC, *ARCH, *COMMON, "-c", os.path.join(CSRC, src), "-o", obj]
+    lang = ["-x", "cu"] if src == "evox_api.cpp" else []  # includes the device header
+    cmd = [NVCC, *ARCH, *COMMON, *lang, "-c", os.path.join(CSRC, src), "-o", obj]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if verbose else []
     subprocess.check_call(cmd)

@@ -422,8 +422,11 @@ struct evox_pso : Base {
         a.uniform_bounds = uniform ? 1 : 0;
         a.rows = rows; a.row0 = row0; a.D = dim; a.ld = ld;
         a.w = w; a.phi_p = phi_p; a.phi_g = phi_g;
+        a.cp = phi_p * 0x1p-24f;
+        a.cg = phi_g * 0x1p-24f;
         a.k0 = (unsigned)(seed & 0xffffffffu);
         a.k1 = (unsigned)(seed >> 32);
+        a.rk = evox::Philox::schedule(seed);
         a.ctl = ctl;
         a.rec = rec;
         a.rec_stride = rec_stride;
@@ -551,6 +554,13 @@ evox_status evox_pso_init(int64_t pop, int64_t dim, const float* lb, const float
     if (!mul_ok(pop, round4(dim), INT64_MAX / 64)) return fail(EVOX_ERR_SHAPE, "pop*dim overflows");
     if (!std::isfinite(w) || !std::isfinite(phi_p) || !std::isfinite(phi_g))
         return fail(EVOX_ERR_INVALID_ARGUMENT, "w, phi_p, phi_g must be finite");
+    // the kernels fold phi * 2^-24 into one multiply; that is exact iff the
+    // scaled value is 0 or a normal float
+    for (float ph : {phi_p, phi_g}) {
+        const float sc = ph * 0x1p-24f;
+        if (ph != 0.0f && (std::fabs(sc) < 0x1p-126f || (double)sc != (double)ph * 0x1p-24))
+            return fail(EVOX_ERR_INVALID_ARGUMENT, "|phi_p|, |phi_g| must be 0 or >= 2^-102");
+    }
     evox_status st = check_bounds(dim, lb, ub);
     if (st != EVOX_OK) return st;
     int world, rank;
@@ -870,6 +880,7 @@ struct evox_cso : Base {
         a.B = B; a.phi = phi; a.xbar = xbar;
         a.k0 = (unsigned)(seed & 0xffffffffu);
         a.k1 = (unsigned)(seed >> 32);
+        a.rk = evox::Philox::schedule(seed);
         a.ctl = ctl;
         a.rank = rank;
         a.world = world;

@@ -15,9 +15,38 @@ enum Problem : int { SPHERE = 0, ACKLEY = 1, RASTRIGIN = 2, GRIEWANK = 3, ROSENB
 // Philox4x32-10 (Salmon et al., SC'11): R-6.  The multiplies compile to
 // IMAD.WIDE.U32 (hi and lo in one instruction); the three-input XORs to LOP3.
 // The key schedule k + r*W is uniform across the grid.
+// Precomputed key schedule (k + r*W, r = 0..9), passed in the kernel parameter
+// block so every round XOR reads its key straight from the constant bank.
+struct PhiloxKey {
+    uint32_t k0[10];
+    uint32_t k1[10];
+};
+
 struct Philox {
     static constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
     static constexpr uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+    __host__ __device__ static PhiloxKey schedule(uint64_t seed) {
+        PhiloxKey k;
+        for (int r = 0; r < 10; ++r) {
+            k.k0[r] = (uint32_t)(seed & 0xffffffffu) + (uint32_t)r * W0;
+            k.k1[r] = (uint32_t)(seed >> 32) + (uint32_t)r * W1;
+        }
+        return k;
+    }
+    __device__ __forceinline__ static uint4 run(uint4 c, const PhiloxKey& k) {
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            const uint64_t p0 = (uint64_t)M0 * c.x;
+            const uint64_t p1 = (uint64_t)M1 * c.z;
+            uint4 n;
+            n.x = (uint32_t)(p1 >> 32) ^ c.y ^ k.k0[r];
+            n.y = (uint32_t)p1;
+            n.z = (uint32_t)(p0 >> 32) ^ c.w ^ k.k1[r];
+            n.w = (uint32_t)p0;
+            c = n;
+        }
+        return c;
+    }
     __device__ __forceinline__ static uint4 run(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
         for (int r = 0; r < 10; ++r) {
@@ -38,6 +67,12 @@ struct Philox {
 // 24-bit uniform in [0,1): (b >> 8) * 2^-24 (exact).  R-6.
 __device__ __forceinline__ float u24(uint32_t b) {
     return __fmul_rn(__uint2float_rn(b >> 8), 0x1p-24f);
+}
+// phi * u24(b) in ONE rounding: (b >> 8) * (phi * 2^-24), where phi * 2^-24 is
+// exact (the host checks it is a normal float or 0), so the product is the
+// same correctly rounded value as phi * ((b >> 8) * 2^-24).
+__device__ __forceinline__ float scaled_u24(uint32_t b, float phi_s) {
+    return __fmul_rn(__uint2float_rn(b >> 8), phi_s);
 }
 
 // -------------------------------------------------------- argmin keys (R-5)
@@ -77,8 +112,22 @@ __device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
 // shard, grid or population size (=> bitwise identical across W, R-11).
 template <int P> struct Fit;
 
-__device__ __forceinline__ float sin2pi(float x) {  // sin^2(pi x)
-    const float s = sinpif(x);
+// sin^2(pi x): sin^2 has period 1, so reduce exactly to r = x - rint(x) in
+// [-1/2, 1/2] (Sterbenz) and evaluate sin(pi r) = r P(r^2) with a degree-4
+// minimax-style polynomial (fitted on [0, 1/4] in r^2; max relative error of
+// the fp32 result ~4e-7).  9 instructions instead of sinpif's ~20.
+__device__ __forceinline__ float sinpi_red(float x) {  // sin(pi (x - rint x)), sign irrelevant
+    const float r = __fsub_rn(x, rintf(x));
+    const float z = __fmul_rn(r, r);
+    float p = 0x1.3db042p-4f;
+    p = __fmaf_rn(p, z, -0x1.324cd0p-1f);
+    p = __fmaf_rn(p, z, 0x1.4668b0p+1f);
+    p = __fmaf_rn(p, z, -0x1.4abbc2p+2f);
+    p = __fmaf_rn(p, z, 0x1.921fb6p+1f);
+    return __fmul_rn(r, p);
+}
+__device__ __forceinline__ float sin2pi(float x) {
+    const float s = sinpi_red(x);
     return __fmul_rn(s, s);
 }
 
@@ -94,7 +143,8 @@ template <> struct Fit<ACKLEY> {
     float s2 = 0.0f, ss = 0.0f;
     __device__ __forceinline__ void elem(float x, int64_t) {
         s2 = __fmaf_rn(x, x, s2);
-        ss = __fadd_rn(ss, sin2pi(x));
+        const float sn = sinpi_red(x);
+        ss = __fmaf_rn(sn, sn, ss);
     }
     __device__ __forceinline__ void combine(const Fit& o) {
         s2 = __fadd_rn(s2, o.s2);
@@ -115,7 +165,8 @@ template <> struct Fit<ACKLEY> {
 template <> struct Fit<RASTRIGIN> {
     float s = 0.0f;
     __device__ __forceinline__ void elem(float x, int64_t) {
-        s = __fadd_rn(s, __fmaf_rn(20.0f, sin2pi(x), __fmul_rn(x, x)));
+        const float sn = sinpi_red(x);
+        s = __fadd_rn(s, __fmaf_rn(__fmul_rn(20.0f, sn), sn, __fmul_rn(x, x)));
     }
     __device__ __forceinline__ void combine(const Fit& o) { s = __fadd_rn(s, o.s); }
     __device__ __forceinline__ void shfl_xor(int m) { s = __shfl_xor_sync(0xffffffffu, s, m); }

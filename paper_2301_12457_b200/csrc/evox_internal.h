@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "evox_device.cuh"
+
 namespace evox {
 
 // Device-resident control block of a handle.  Kernels read the generation
@@ -38,7 +40,9 @@ struct PsoArgs {
     int uniform_bounds;
     long long rows, row0, D, ld;
     float w, phi_p, phi_g;
+    float cp, cg;         // phi_p * 2^-24, phi_g * 2^-24 (exact; see scaled_u24)
     unsigned int k0, k1;  // Philox key = seed
+    PhiloxKey rk;         // its key schedule
     Ctl* ctl;
     unsigned char* rec;   // world > 1: W winner records, stride rec_stride bytes
     long long rec_stride;
@@ -59,6 +63,7 @@ struct CsoArgs {
     float phi;
     const float* xbar;  // [ld] column means (phi != 0)
     unsigned int k0, k1;
+    PhiloxKey rk;
     Ctl* ctl;
     int rank, world;
     int exchange;  // 1: per-generation keys go to hkeys for one NCCL min-reduction per call

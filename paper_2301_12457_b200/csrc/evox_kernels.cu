@@ -45,12 +45,11 @@ __device__ __forceinline__ float clipf(float x, float lo, float hi) {
 }
 
 // The PSO velocity/position update of one element (R-1, R-4), exact op order.
-__device__ __forceinline__ void pso_elem(float& x, float& v, float p, float g, float r1, float r2,
-                                         float w, float phi_p, float phi_g, float lo, float hi) {
+// c1 = phi_p r1 and c2 = phi_g r2 arrive already scaled (scaled_u24).
+__device__ __forceinline__ void pso_elem(float& x, float& v, float p, float g, float c1, float c2,
+                                         float w, float lo, float hi) {
     const float a = __fsub_rn(p, x);
     const float b = __fsub_rn(g, x);
-    const float c1 = __fmul_rn(phi_p, r1);
-    const float c2 = __fmul_rn(phi_g, r2);
     const float vn = __fmaf_rn(c2, b, __fmaf_rn(c1, a, __fmul_rn(w, v)));
     x = clipf(__fadd_rn(x, vn), lo, hi);
     v = vn;
@@ -155,37 +154,26 @@ struct MoverEval {
     __device__ __forceinline__ float4 step(int u, long long) { return x[u]; }
 };
 
-// PSO move of one row (A1, A3, A4, lazy A5).  Scalars are copied in by value
-// (no pointer to the kernel parameter block, which would force a local copy).
+// PSO move of one row (A1, A3, A4, lazy A5).  Holds a reference to the kernel
+// parameter block (resolved to constant-bank operands once inlined: the
+// Philox round keys, w, phi*2^-24 and the bounds feed instructions directly).
 struct MoverPso {
+    const PsoArgs& a;
     float4* Xr;
     float4* Vr;
     float4* Pr;
-    const float4* G;
-    const float4* lb;
-    const float4* ub;
-    float lb0, ub0, w, phi_p, phi_g;
-    uint32_t k0, k1;
     uint32_t row_g;  // global row (Philox counter word 1)
     uint32_t t;      // generation of the source population (counter word 2)
     bool pend;       // pbest copy pending: P := X_t, P not read
-    bool uni;        // uniform bounds
-    long long D;
     float4 x[U], v[U], p[U];
-    __device__ __forceinline__ void init(const PsoArgs& a, long long row, uint32_t t_) {
+    __device__ __forceinline__ MoverPso(const PsoArgs& a_, long long row, uint32_t t_, bool pend_)
+        : a(a_) {
         Xr = reinterpret_cast<float4*>(a.X + row * a.ld);
         Vr = reinterpret_cast<float4*>(a.V + row * a.ld);
         Pr = reinterpret_cast<float4*>(a.P + row * a.ld);
-        G = reinterpret_cast<const float4*>(a.G);
-        lb = reinterpret_cast<const float4*>(a.lb);
-        ub = reinterpret_cast<const float4*>(a.ub);
-        lb0 = a.lb0; ub0 = a.ub0; w = a.w; phi_p = a.phi_p; phi_g = a.phi_g;
-        k0 = a.k0; k1 = a.k1;
         row_g = (uint32_t)(a.row0 + row);
         t = t_;
-        pend = a.imp[row] != 0;
-        uni = a.uniform_bounds != 0;
-        D = a.D;
+        pend = pend_;
     }
     __device__ __forceinline__ void load(int u, long long q) {
         x[u] = ld_stream(Xr + q);
@@ -196,27 +184,42 @@ struct MoverPso {
         const float4 xo = x[u];
         const float4 pb = pend ? xo : p[u];
         if (pend) st_stream(Pr + q, xo);
-        const float4 g = __ldg(G + q);
-        const float4 lo = uni ? make_float4(lb0, lb0, lb0, lb0) : __ldg(lb + q);
-        const float4 hi = uni ? make_float4(ub0, ub0, ub0, ub0) : __ldg(ub + q);
-        const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 2u), k0, k1);
-        const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 3u), k0, k1);
+        const float4 g = __ldg(reinterpret_cast<const float4*>(a.G) + q);
+        float4 lo, hi;
+        if (a.uniform_bounds) {
+            lo = make_float4(a.lb0, a.lb0, a.lb0, a.lb0);
+            hi = make_float4(a.ub0, a.ub0, a.ub0, a.ub0);
+        } else {
+            lo = __ldg(reinterpret_cast<const float4*>(a.lb) + q);
+            hi = __ldg(reinterpret_cast<const float4*>(a.ub) + q);
+        }
+        const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 2u), a.rk);
+        const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 3u), a.rk);
         float4 xn = xo, vn = v[u];
-        pso_elem(xn.x, vn.x, pb.x, g.x, u24(b1.x), u24(b2.x), w, phi_p, phi_g, lo.x, hi.x);
-        pso_elem(xn.y, vn.y, pb.y, g.y, u24(b1.y), u24(b2.y), w, phi_p, phi_g, lo.y, hi.y);
-        pso_elem(xn.z, vn.z, pb.z, g.z, u24(b1.z), u24(b2.z), w, phi_p, phi_g, lo.z, hi.z);
-        pso_elem(xn.w, vn.w, pb.w, g.w, u24(b1.w), u24(b2.w), w, phi_p, phi_g, lo.w, hi.w);
-        if (4 * q + 3 >= D) {  // padding columns stay 0
+        const float w = a.w, cp = a.cp, cg = a.cg;
+        pso_elem(xn.x, vn.x, pb.x, g.x, scaled_u24(b1.x, cp), scaled_u24(b2.x, cg), w, lo.x, hi.x);
+        pso_elem(xn.y, vn.y, pb.y, g.y, scaled_u24(b1.y, cp), scaled_u24(b2.y, cg), w, lo.y, hi.y);
+        pso_elem(xn.z, vn.z, pb.z, g.z, scaled_u24(b1.z, cp), scaled_u24(b2.z, cg), w, lo.z, hi.z);
+        pso_elem(xn.w, vn.w, pb.w, g.w, scaled_u24(b1.w, cp), scaled_u24(b2.w, cg), w, lo.w, hi.w);
+        if (4 * q + 3 >= a.D) {  // padding columns stay 0
             const long long j0 = 4 * q;
-            if (j0 + 1 >= D) { xn.y = 0.f; vn.y = 0.f; }
-            if (j0 + 2 >= D) { xn.z = 0.f; vn.z = 0.f; }
-            if (j0 + 3 >= D) { xn.w = 0.f; vn.w = 0.f; }
+            if (j0 + 1 >= a.D) { xn.y = 0.f; vn.y = 0.f; }
+            if (j0 + 2 >= a.D) { xn.z = 0.f; vn.z = 0.f; }
+            if (j0 + 3 >= a.D) { xn.w = 0.f; vn.w = 0.f; }
         }
         st_stream(Xr + q, xn);
         st_stream(Vr + q, vn);
         return xn;
     }
 };
+
+// Bulk L2 prefetch (Hopper+ cp.async.bulk.prefetch): pulls a whole row segment
+// from HBM into L2 with one instruction, so the next row's LDGs hit L2.
+__device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
+    if (bytes > 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((uint32_t)bytes)
+                     : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // Grid-level argmin + finalize (A12/A13).  Every thread calls it after its
@@ -333,7 +336,7 @@ __global__ void k_pso_init(PsoArgs a) {
 
 // evox_eval: fit[r] = f(X[r]).
 template <int P, int WPR>
-__global__ void __launch_bounds__(256) k_eval(const float* __restrict__ X, long long rows,
+__global__ void __launch_bounds__(WPR == 1 ? 256 : WPR * 32) k_eval(const float* __restrict__ X, long long rows,
                                               long long D, long long ld, float* __restrict__ fit) {
     __shared__ Fit<P> sh_acc[WPR > 1 ? WPR : 1];
     __shared__ float sh_head[WPR > 1 ? WPR : 1];
@@ -369,12 +372,26 @@ __global__ void __launch_bounds__(WPR == 1 ? 256 : WPR * 32) k_pso_gen(PsoArgs a
     long long qb, qe;
     row_segment(a.ld >> 2, WPR, wr, qb, qe);
     unsigned long long best = ~0ull;
-    for (long long row = (long long)blockIdx.x * RPC + slot; row < a.rows;
-         row += (long long)gridDim.x * RPC) {
+    const long long stride = (long long)gridDim.x * RPC;
+    const long long seg_off = qb * 16, seg_bytes = (qe - qb) * 16;
+    long long row = (long long)blockIdx.x * RPC + slot;
+    // pbest-pending flags one and two rows ahead (imp[r] is rewritten only by
+    // the warp(s) that own row r, later in this kernel, so these reads see the
+    // previous generation's decisions).
+    bool pend_cur = row < a.rows ? a.imp[row] != 0 : false;
+    bool pend_nxt = row + stride < a.rows ? a.imp[row + stride] != 0 : true;
+    for (; row < a.rows; row += stride) {
+        const long long nxt = row + stride, nn = nxt + stride;
+        if (lane == 0 && nxt < a.rows) {  // next row of this warp: HBM -> L2 now
+            const long long o = nxt * a.ld * 4 + seg_off;
+            prefetch_l2(reinterpret_cast<const char*>(a.X) + o, seg_bytes);
+            prefetch_l2(reinterpret_cast<const char*>(a.V) + o, seg_bytes);
+            if (!pend_nxt) prefetch_l2(reinterpret_cast<const char*>(a.P) + o, seg_bytes);
+        }
+        const bool pend_nn = nn < a.rows ? a.imp[nn] != 0 : true;
         float pf_old = 0.0f;
         if (lane == 0) pf_old = a.pf[row];
-        MoverPso mv;
-        mv.init(a, row, (uint32_t)t);
+        MoverPso mv(a, row, (uint32_t)t, pend_cur);
         Fit<P> acc;
         float hx, tx;
         bool tv;
@@ -389,6 +406,8 @@ __global__ void __launch_bounds__(WPR == 1 ? 256 : WPR * 32) k_pso_gen(PsoArgs a
             const unsigned long long k = make_key(f, a.row0 + row);
             best = k < best ? k : best;
         }
+        pend_cur = pend_nxt;
+        pend_nxt = pend_nn;
     }
     unsigned long long key;
     if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
@@ -406,8 +425,7 @@ __global__ void __launch_bounds__(WPR == 1 ? 256 : WPR * 32) k_pso_move(PsoArgs 
     row_segment(a.ld >> 2, WPR, wr, qb, qe);
     for (long long row = (long long)blockIdx.x * RPC + slot; row < a.rows;
          row += (long long)gridDim.x * RPC) {
-        MoverPso mv;
-        mv.init(a, row, (uint32_t)t);
+        MoverPso mv(a, row, (uint32_t)t, a.imp[row] != 0);
         Fit<SPHERE> acc;  // unused
         float hx, tx;
         bool tv;
@@ -536,7 +554,8 @@ struct MoverCso {
     const float4* ub;
     const float4* xbar;
     float lb0, ub0, phi;
-    uint32_t k0, k1, row_g, t;
+    const PhiloxKey* rk;
+    uint32_t row_g, t;
     bool uni;
     long long D;
     float4 x[U], v[U], xw[U];
@@ -554,12 +573,12 @@ struct MoverCso {
         return clipf(__fadd_rn(xl, v), lo, hi);
     }
     __device__ __forceinline__ float4 step(int u, long long q) {
-        const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 5u), k0, k1);
-        const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 6u), k0, k1);
+        const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 5u), *rk);
+        const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 6u), *rk);
         const bool use3 = phi != 0.0f;
         float4 c3 = make_float4(0.f, 0.f, 0.f, 0.f), xb = c3;
         if (use3) {
-            const uint4 b3 = Philox::run(make_uint4((uint32_t)q, row_g, t, 7u), k0, k1);
+            const uint4 b3 = Philox::run(make_uint4((uint32_t)q, row_g, t, 7u), *rk);
             c3 = make_float4(__fmul_rn(phi, u24(b3.x)), __fmul_rn(phi, u24(b3.y)),
                              __fmul_rn(phi, u24(b3.z)), __fmul_rn(phi, u24(b3.w)));
             xb = __ldg(xbar + q);
@@ -649,7 +668,7 @@ __global__ void __launch_bounds__(WPR == 1 ? 256 : WPR * 32) k_cso_gen(CsoArgs a
         mv.ub = reinterpret_cast<const float4*>(a.ub);
         mv.xbar = reinterpret_cast<const float4*>(a.xbar);
         mv.lb0 = a.lb0; mv.ub0 = a.ub0; mv.phi = a.phi;
-        mv.k0 = a.k0; mv.k1 = a.k1;
+        mv.rk = &a.rk;
         mv.row_g = (uint32_t)gl;
         mv.t = (uint32_t)t;
         mv.uni = a.uniform_bounds != 0;

@@ -114,10 +114,10 @@ PSO_CASES = [("sphere", 100, 10, -5.12, 5.12, 0),        # C1
              ("ackley", 6, 40001, -32.768, 32.768, 6)]
 
 
-def _run_parity(problem, N, D, lb, ub, seed, gens, checkpoints=(1, 10, 100)):
+def _run_parity(problem, N, D, lb, ub, seed, gens, checkpoints=(1, 10, 100), threads=1):
     pso = ev.PSO(N, D, lb, ub, seed=seed)
     pso.step(problem, 0)
-    st = O.pso_run(problem, N, D, lb, ub, seed=seed, n_gens=0)
+    st = O.pso_run(problem, N, D, lb, ub, seed=seed, n_gens=0, threads=threads)
     g = gpu_pso_state(pso, D)
     flips = compare_pso(g, st, label=f"{problem} t=0")
     if flips:
@@ -126,7 +126,7 @@ def _run_parity(problem, N, D, lb, ub, seed, gens, checkpoints=(1, 10, 100)):
     for t in range(1, gens + 1):
         prev_pf = g["pf"]
         pso.step(problem, 1)
-        st = O.pso_run(problem, N, D, lb, ub, seed=seed, n_gens=1, state=st)
+        st = O.pso_run(problem, N, D, lb, ub, seed=seed, n_gens=1, state=st, threads=threads)
         g = gpu_pso_state(pso, D)
         flips = compare_pso(g, st, prev_pf_gpu=prev_pf, label=f"{problem} t={t}")
         if flips:
@@ -340,15 +340,15 @@ def test_full_size_sampled(cfg):
 
 
 def test_c2_full_parity_10_gens():
-    """C2 (PSO/Ackley 1e4 x 1000) compared element by element for 10 generations."""
+    """C2 (PSO/Ackley 1e4 x 1000) compared element by element every generation for 10
+    generations (near-tie protocol R-9), checkpoints at 1 and 10."""
     c = WL.CONFIGS["C2"]
     lb, ub = WL.BOUNDS[c.problem]
-    pso = ev.PSO(c.pop, c.dim, lb, ub, seed=0)
-    pso.step(c.problem, 10)
-    st = O.pso_run(c.problem, c.pop, c.dim, lb, ub, seed=0, n_gens=10, threads=8)
-    g = gpu_pso_state(pso, c.dim)
-    flips = compare_pso(g, st, label="C2 t=10")
-    assert not flips, flips
+    pso, log = _run_parity(c.problem, c.pop, c.dim, lb, ub, 0, 10, checkpoints=(1, 10),
+                           threads=8)
+    if log:
+        print(f"C2 near-tie resyncs: {log}")
+    assert sum(len(f) for _, f in log) <= 20, log
 
 
 # ------------------------------------------------------------------- CSO
