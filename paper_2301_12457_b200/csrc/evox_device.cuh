@@ -135,7 +135,7 @@ template <> struct Fit<SPHERE> {
     float s = 0.0f;
     __device__ __forceinline__ void elem(float x, int64_t) { s = __fmaf_rn(x, x, s); }
     __device__ __forceinline__ void combine(const Fit& o) { s = __fadd_rn(s, o.s); }
-    __device__ __forceinline__ void shfl_xor(int m) { s = __shfl_xor_sync(0xffffffffu, s, m); }
+    __device__ __forceinline__ void shfl_xor(int m, int w) { s = __shfl_xor_sync(0xffffffffu, s, m, w); }
     __device__ __forceinline__ float finish(int64_t) const { return s; }
 };
 
@@ -150,9 +150,9 @@ template <> struct Fit<ACKLEY> {
         s2 = __fadd_rn(s2, o.s2);
         ss = __fadd_rn(ss, o.ss);
     }
-    __device__ __forceinline__ void shfl_xor(int m) {
-        s2 = __shfl_xor_sync(0xffffffffu, s2, m);
-        ss = __shfl_xor_sync(0xffffffffu, ss, m);
+    __device__ __forceinline__ void shfl_xor(int m, int w) {
+        s2 = __shfl_xor_sync(0xffffffffu, s2, m, w);
+        ss = __shfl_xor_sync(0xffffffffu, ss, m, w);
     }
     __device__ __forceinline__ float finish(int64_t D) const {
         const float invD = __frcp_rn((float)D);
@@ -169,26 +169,33 @@ template <> struct Fit<RASTRIGIN> {
         s = __fadd_rn(s, __fmaf_rn(__fmul_rn(20.0f, sn), sn, __fmul_rn(x, x)));
     }
     __device__ __forceinline__ void combine(const Fit& o) { s = __fadd_rn(s, o.s); }
-    __device__ __forceinline__ void shfl_xor(int m) { s = __shfl_xor_sync(0xffffffffu, s, m); }
+    __device__ __forceinline__ void shfl_xor(int m, int w) { s = __shfl_xor_sync(0xffffffffu, s, m, w); }
     __device__ __forceinline__ float finish(int64_t) const { return s; }
 };
 
+// Griewank: a_j = 1 - cos(x_j / sqrt(j+1)) = 2 sin^2(pi z), z = x_j h_j with
+// h_j = 1 / (2 pi sqrt(j+1)) (per-column constant: from the CTA's shared-memory
+// table when one exists, else computed with a correctly rounded rsqrt).
+__device__ __forceinline__ float griewank_h(int64_t j) {
+    return __fmul_rn(0.15915494309189535f, __frsqrt_rn((float)(j + 1)));
+}
+
 template <> struct Fit<GRIEWANK> {
     float s2 = 0.0f, q = 0.0f;
-    __device__ __forceinline__ void elem(float x, int64_t j) {
+    __device__ __forceinline__ void term(float x, float h) {
         s2 = __fmaf_rn(x, x, s2);
-        const float h = __fmul_rn(0.5f, __frsqrt_rn((float)(j + 1)));  // 1/(2 sqrt(j+1))
-        const float sn = sinf(__fmul_rn(x, h));
+        const float sn = sinpi_red(__fmul_rn(x, h));
         const float a = __fmul_rn(2.0f, __fmul_rn(sn, sn));  // 1 - cos(x/sqrt(j+1))
-        q = __fmaf_rn(-q, a, __fadd_rn(q, a));
+        q = __fmaf_rn(-q, a, __fadd_rn(q, a));               // complement product
     }
+    __device__ __forceinline__ void elem(float x, int64_t j) { term(x, griewank_h(j)); }
     __device__ __forceinline__ void combine(const Fit& o) {
         s2 = __fadd_rn(s2, o.s2);
         q = __fmaf_rn(-q, o.q, __fadd_rn(q, o.q));
     }
-    __device__ __forceinline__ void shfl_xor(int m) {
-        s2 = __shfl_xor_sync(0xffffffffu, s2, m);
-        q = __shfl_xor_sync(0xffffffffu, q, m);
+    __device__ __forceinline__ void shfl_xor(int m, int w) {
+        s2 = __shfl_xor_sync(0xffffffffu, s2, m, w);
+        q = __shfl_xor_sync(0xffffffffu, q, m, w);
     }
     __device__ __forceinline__ float finish(int64_t) const {
         return __fadd_rn(__fmul_rn(s2, 1.0f / 4000.0f), q);
@@ -204,7 +211,7 @@ template <> struct Fit<ROSENBROCK> {
         s = __fadd_rn(s, __fmaf_rn(__fmul_rn(100.0f, d), d, __fmul_rn(e, e)));
     }
     __device__ __forceinline__ void combine(const Fit& o) { s = __fadd_rn(s, o.s); }
-    __device__ __forceinline__ void shfl_xor(int m) { s = __shfl_xor_sync(0xffffffffu, s, m); }
+    __device__ __forceinline__ void shfl_xor(int m, int w) { s = __shfl_xor_sync(0xffffffffu, s, m, w); }
     __device__ __forceinline__ float finish(int64_t) const { return s; }
 };
 
@@ -212,7 +219,8 @@ template <> struct Fit<ROSENBROCK> {
 // folds the three intra-quad pairs (the pair crossing into the next quad is
 // handled by the row engine with a shuffle / carried value).
 template <int P>
-__device__ __forceinline__ void fit_quad(Fit<P>& acc, float4 x, int64_t j0, int64_t D) {
+__device__ __forceinline__ void fit_quad(Fit<P>& acc, float4 x, int64_t j0, int64_t D,
+                                         const float* = nullptr) {
     if (j0 + 3 < D) {
         acc.elem(x.x, j0); acc.elem(x.y, j0 + 1); acc.elem(x.z, j0 + 2); acc.elem(x.w, j0 + 3);
     } else {
@@ -222,8 +230,26 @@ __device__ __forceinline__ void fit_quad(Fit<P>& acc, float4 x, int64_t j0, int6
     }
 }
 template <>
+__device__ __forceinline__ void fit_quad<GRIEWANK>(Fit<GRIEWANK>& acc, float4 x, int64_t j0,
+                                                   int64_t D, const float* htab) {
+    float4 h;
+    if (htab) {
+        h = *reinterpret_cast<const float4*>(htab + j0);  // LDS.128 of the column constants
+    } else {
+        h = make_float4(griewank_h(j0), griewank_h(j0 + 1), griewank_h(j0 + 2),
+                        griewank_h(j0 + 3));
+    }
+    if (j0 + 3 < D) {
+        acc.term(x.x, h.x); acc.term(x.y, h.y); acc.term(x.z, h.z); acc.term(x.w, h.w);
+    } else {
+        if (j0 < D) acc.term(x.x, h.x);
+        if (j0 + 1 < D) acc.term(x.y, h.y);
+        if (j0 + 2 < D) acc.term(x.z, h.z);
+    }
+}
+template <>
 __device__ __forceinline__ void fit_quad<ROSENBROCK>(Fit<ROSENBROCK>& acc, float4 x, int64_t j0,
-                                                     int64_t D) {
+                                                     int64_t D, const float*) {
     if (j0 + 1 < D) acc.pair(x.x, x.y);
     if (j0 + 2 < D) acc.pair(x.y, x.z);
     if (j0 + 3 < D) acc.pair(x.z, x.w);

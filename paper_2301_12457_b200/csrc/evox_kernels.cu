@@ -7,10 +7,17 @@
 // generation's argmin (warp -> CTA -> one atomicMin per CTA); the last CTA to
 // finish publishes gbest.  20 B/element of HBM traffic per generation.
 //
-// Row mapping: WPR warps per row (a function of dim only).  Each warp owns a
-// contiguous segment of the row's float4 quads and walks it in chunks of 32
-// quads (one LDG.128/STG.128 per lane per array per chunk, 512 B per warp
-// instruction), U chunks in flight.
+// Row engine geometry (a function of ld only, so every result is bitwise the
+// same for every shard count, R-11):
+//   * LPR lanes walk one row (LPR = 8 for ld <= 256, else 32); a warp holds
+//     RPW = 32/LPR consecutive rows; or
+//   * WPR = 8 warps (one CTA) share one row, each owning a contiguous segment
+//     (ld > 4096).
+// Lanes walk their segment in chunks of LPR float4 quads (one LDG.128/STG.128
+// per lane per array per chunk), U chunks in flight.  The HBM stream is kept
+// ahead of the loads with cp.async.bulk.prefetch.L2 (SASS UBLKPF): the next
+// rows of the warp when they are short (mode A), or a sliding window of
+// AHEAD quads inside long rows (mode B).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -22,17 +29,29 @@ namespace evox {
 
 namespace {
 
-constexpr int U = 4;  // chunks (of 32 quads) in flight per warp
+constexpr int U = 4;               // chunks in flight per lane group
+constexpr int WARPS = 8;           // warps per CTA (256 threads) in every geometry
+constexpr long long MODE_A_MAX = 384;  // quads per warp-iteration prefetched whole (mode A)
+constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
-// Row segment of warp `wr` (of WPR) over NQ quads.
+template <int LPR_, int WPR_>
+struct Geom {
+    static constexpr int LPR = LPR_;              // lanes per row segment
+    static constexpr int WPR = WPR_;              // warps per row
+    static constexpr int RPW = 32 / LPR_;         // rows per warp (WPR == 1)
+    static constexpr int RPC = WPR_ == 1 ? WARPS * RPW : WARPS / WPR_;  // rows per CTA pass
+    static constexpr int GROUP = LPR_ * U;        // quads per lane-group iteration
+};
+
+// Row segment [qb, qe) of warp `wr` (of WPR) over NQ quads.
 __device__ __forceinline__ void row_segment(long long NQ, int wpr, int wr, long long& qb,
                                             long long& qe) {
     const long long seg = (NQ + wpr - 1) / wpr;
     qb = (long long)wr * seg;
-    qe = qb + seg < NQ ? qb + seg : NQ;
     if (qb > NQ) qb = NQ;
+    qe = qb + seg < NQ ? qb + seg : NQ;
 }
 
 __device__ __forceinline__ float4 bound4(const float* b, float b0, int uniform, long long q) {
@@ -42,6 +61,14 @@ __device__ __forceinline__ float4 bound4(const float* b, float b0, int uniform, 
 
 __device__ __forceinline__ float clipf(float x, float lo, float hi) {
     return fminf(fmaxf(x, lo), hi);
+}
+
+// Bulk L2 prefetch (Hopper+ cp.async.bulk.prefetch): pulls a whole run of a row
+// from HBM into L2 with one instruction, so later LDGs of it hit L2.
+__device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
+    if (bytes > 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((uint32_t)bytes)
+                     : "memory");
 }
 
 // The PSO velocity/position update of one element (R-1, R-4), exact op order.
@@ -55,47 +82,92 @@ __device__ __forceinline__ void pso_elem(float& x, float& v, float p, float g, f
     v = vn;
 }
 
+__device__ __forceinline__ void zero_pad(float4& x, float4& v, long long q, long long D) {
+    if (4 * q + 3 >= D) {  // padding columns stay 0
+        const long long j0 = 4 * q;
+        if (j0 + 1 >= D) { x.y = 0.f; v.y = 0.f; }
+        if (j0 + 2 >= D) { x.z = 0.f; v.z = 0.f; }
+        if (j0 + 3 >= D) { x.w = 0.f; v.w = 0.f; }
+    }
+}
+
+// Griewank column constants h_j = 1/(2 pi sqrt(j+1)) for one CTA, computed in
+// fp64 and rounded once (geometries with ld <= HTAB; else computed per element).
+constexpr int HTAB = 4096;
+template <int P, class G>
+struct HTable {
+    __device__ __forceinline__ static const float* fill(float*, long long) { return nullptr; }
+};
+template <class G>
+struct HTable<GRIEWANK, G> {
+    __device__ __forceinline__ static const float* fill(float* sh, long long ld) {
+        if (G::WPR > 1 || ld > HTAB) return nullptr;
+        for (long long j = threadIdx.x; j < ld; j += blockDim.x)
+            sh[j] = (float)(0.15915494309189534 / sqrt((double)(j + 1)));
+        __syncthreads();
+        return sh;
+    }
+};
+template <int P>
+struct HStore {
+    float v[1];
+};
+template <>
+struct HStore<GRIEWANK> {
+    float v[HTAB];
+};
+
+struct NoPrefetch {
+    __device__ __forceinline__ void operator()(long long) {}
+};
+
 // ---------------------------------------------------------------------------
-// Row engine: walks one row segment chunk by chunk; `mv` loads/moves a quad
-// and returns the value to evaluate; folds the fitness (with the Rosenbrock
-// cross-quad halo).  All lanes of the warp execute every chunk iteration.
-template <int P, class Mover>
+// Row engine: walks one row segment [qb, qe) chunk by chunk; `mv` loads/moves a
+// quad and returns the value to evaluate; folds the fitness (with the
+// Rosenbrock cross-quad halo).  Every lane of the warp executes every chunk
+// iteration (qb/qe are warp-uniform); lanes of an absent row (`row_ok` false)
+// do no memory work.  `pf(base)` is called by the warp at each group start.
+template <int P, class G, class Mover, class PF>
 __device__ __forceinline__ void walk_segment(Mover& mv, long long qb, long long qe, long long D,
-                                             Fit<P>& acc, float& head_x, float& tail_x,
-                                             bool& tail_valid) {
-    const int lane = lane_id();
+                                             bool row_ok, Fit<P>& acc, float& head_x,
+                                             float& tail_x, bool& tail_valid, PF& pf,
+                                             const float* htab = nullptr) {
+    const int sl = lane_id() & (G::LPR - 1);
     float pend_x = 0.0f;
-    bool pend = false;  // lane 31: x_{4q+3} waiting for x_{4q+4} of the next chunk
+    bool pend = false;  // last sub-lane: x_{4q+3} waiting for x_{4q+4} of the next chunk
     head_x = 0.0f;
     tail_valid = false;
     tail_x = 0.0f;
-    for (long long base = qb; base < qe; base += 32 * U) {
+    for (long long base = qb; base < qe; base += G::GROUP) {
+        pf(base);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const long long q = base + 32 * u + lane;
-            if (q < qe) mv.load(u, q);
+            const long long q = base + G::LPR * u + sl;
+            if (row_ok && q < qe) mv.load(u, q);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const long long cb = base + 32 * u;  // first quad of this chunk
-            if (cb >= qe) break;                 // warp-uniform
-            const long long q = cb + lane;
-            const bool valid = q < qe;
+            const long long cb = base + G::LPR * u;  // first quad of this chunk
+            if (cb >= qe) break;                     // warp-uniform
+            const long long q = cb + sl;
+            const bool valid = row_ok && q < qe;
             float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid) xn = mv.step(u, q);
-            if (valid) fit_quad<P>(acc, xn, 4 * q, D);
+            if (valid) {
+                xn = mv.step(u, q);
+                fit_quad<P>(acc, xn, 4 * q, D, htab);
+            }
             if constexpr (P == ROSENBROCK) {
-                const float nb = __shfl_down_sync(0xffffffffu, xn.x, 1);
-                const float f0 = __shfl_sync(0xffffffffu, xn.x, 0);
+                const float nb = __shfl_down_sync(FULL, xn.x, 1, G::LPR);
+                const float f0 = __shfl_sync(FULL, xn.x, 0, G::LPR);
                 if (cb == qb) head_x = f0;
-                if (lane == 31 && pend) {
+                if (sl == G::LPR - 1 && pend) {
                     acc.pair(pend_x, f0);
                     pend = false;
                 }
                 if (valid) {
                     const bool has_next = 4 * q + 4 < D;
                     if (q + 1 < qe) {
-                        if (lane < 31) {
+                        if (sl < G::LPR - 1) {
                             if (has_next) acc.pair(xn.w, nb);
                         } else {
                             pend = has_next;
@@ -111,39 +183,70 @@ __device__ __forceinline__ void walk_segment(Mover& mv, long long qb, long long 
     }
 }
 
-// Reduce a row's fitness over the warp (xor tree) and, for WPR > 1, over the
-// row's warps in fixed order through shared memory.  Returns f in lane 0 of
-// warp 0 of the row group (other threads: unspecified).
-template <int P, int WPR>
+// Reduce a row's fitness over its lanes (xor butterfly of width LPR) and, for
+// WPR > 1, over the row's warps in fixed order through shared memory.  Returns
+// f in sub-lane 0 (WPR == 1) / thread 0 (WPR > 1).
+template <int P, class G>
 __device__ __forceinline__ float reduce_row(Fit<P> acc, long long D, float head_x, float tail_x,
                                             bool tail_valid, Fit<P>* sh_acc, float* sh_head) {
     const int lane = lane_id();
-    if constexpr (WPR > 1 && P == ROSENBROCK) {
+    if constexpr (G::WPR > 1 && P == ROSENBROCK) {
         const int wr = threadIdx.x >> 5;
         if (lane == 0) sh_head[wr] = head_x;
         __syncthreads();
-        if (tail_valid && wr + 1 < WPR) acc.pair(tail_x, sh_head[wr + 1]);
+        if (tail_valid && wr + 1 < G::WPR) acc.pair(tail_x, sh_head[wr + 1]);
     }
 #pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
+    for (int m = G::LPR / 2; m >= 1; m >>= 1) {
         Fit<P> o = acc;
-        o.shfl_xor(m);
+        o.shfl_xor(m, G::LPR);
         acc.combine(o);
     }
-    if constexpr (WPR == 1) return acc.finish(D);
-    const int wr = threadIdx.x >> 5;
-    if (lane == 0) sh_acc[wr] = acc;
-    __syncthreads();
-    float f = 0.0f;
-    if (threadIdx.x == 0) {
-        Fit<P> t = sh_acc[0];
+    if constexpr (G::WPR == 1) {
+        return acc.finish(D);
+    } else {
+        const int wr = threadIdx.x >> 5;
+        if (lane == 0) sh_acc[wr] = acc;
+        __syncthreads();
+        float f = 0.0f;
+        if (threadIdx.x == 0) {
+            Fit<P> t = sh_acc[0];
 #pragma unroll 1
-        for (int k = 1; k < WPR; ++k) t.combine(sh_acc[k]);
-        f = t.finish(D);
+            for (int k = 1; k < G::WPR; ++k) t.combine(sh_acc[k]);
+            f = t.finish(D);
+        }
+        __syncthreads();  // sh_acc / sh_head reusable for the next row
+        return f;
     }
-    __syncthreads();  // sh_acc / sh_head reusable for the next row
-    return f;
 }
+
+// Thread-to-row mapping of a geometry.
+template <class G>
+struct RowMap {
+    long long first, stride;  // this thread's first row and the row stride per iteration
+    long long wfirst;         // the warp's first row (WPR == 1: rows wfirst..wfirst+RPW-1)
+    int sl;                   // sub-lane within the row group
+    bool leader;              // the thread that owns the row's scalar results
+    long long qb, qe;         // this warp's segment of the row
+    __device__ __forceinline__ RowMap(long long NQ) {
+        const int wid = threadIdx.x >> 5, lane = lane_id();
+        sl = lane & (G::LPR - 1);
+        if constexpr (G::WPR == 1) {
+            wfirst = ((long long)blockIdx.x * WARPS + wid) * G::RPW;
+            first = wfirst + lane / G::LPR;
+            stride = (long long)gridDim.x * G::RPC;
+            leader = sl == 0;
+            qb = 0;
+            qe = NQ;
+        } else {
+            wfirst = (long long)blockIdx.x * (WARPS / G::WPR) + wid / G::WPR;
+            first = wfirst;
+            stride = (long long)gridDim.x * G::RPC;
+            leader = (threadIdx.x % (G::WPR * 32)) == 0;
+            row_segment(NQ, G::WPR, wid % G::WPR, qb, qe);
+        }
+    }
+};
 
 // ---------------------------------------------------------------------------
 // Movers
@@ -185,14 +288,8 @@ struct MoverPso {
         const float4 pb = pend ? xo : p[u];
         if (pend) st_stream(Pr + q, xo);
         const float4 g = __ldg(reinterpret_cast<const float4*>(a.G) + q);
-        float4 lo, hi;
-        if (a.uniform_bounds) {
-            lo = make_float4(a.lb0, a.lb0, a.lb0, a.lb0);
-            hi = make_float4(a.ub0, a.ub0, a.ub0, a.ub0);
-        } else {
-            lo = __ldg(reinterpret_cast<const float4*>(a.lb) + q);
-            hi = __ldg(reinterpret_cast<const float4*>(a.ub) + q);
-        }
+        const float4 lo = bound4(a.lb, a.lb0, a.uniform_bounds, q);
+        const float4 hi = bound4(a.ub, a.ub0, a.uniform_bounds, q);
         const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 2u), a.rk);
         const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 3u), a.rk);
         float4 xn = xo, vn = v[u];
@@ -201,39 +298,62 @@ struct MoverPso {
         pso_elem(xn.y, vn.y, pb.y, g.y, scaled_u24(b1.y, cp), scaled_u24(b2.y, cg), w, lo.y, hi.y);
         pso_elem(xn.z, vn.z, pb.z, g.z, scaled_u24(b1.z, cp), scaled_u24(b2.z, cg), w, lo.z, hi.z);
         pso_elem(xn.w, vn.w, pb.w, g.w, scaled_u24(b1.w, cp), scaled_u24(b2.w, cg), w, lo.w, hi.w);
-        if (4 * q + 3 >= a.D) {  // padding columns stay 0
-            const long long j0 = 4 * q;
-            if (j0 + 1 >= a.D) { xn.y = 0.f; vn.y = 0.f; }
-            if (j0 + 2 >= a.D) { xn.z = 0.f; vn.z = 0.f; }
-            if (j0 + 3 >= a.D) { xn.w = 0.f; vn.w = 0.f; }
-        }
+        zero_pad(xn, vn, q, a.D);
         st_stream(Xr + q, xn);
         st_stream(Vr + q, vn);
         return xn;
     }
 };
 
-// Bulk L2 prefetch (Hopper+ cp.async.bulk.prefetch): pulls a whole row segment
-// from HBM into L2 with one instruction, so the next row's LDGs hit L2.
-__device__ __forceinline__ void prefetch_l2(const void* p, long long bytes) {
-    if (bytes > 0)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((uint32_t)bytes)
-                     : "memory");
-}
+// Mode-B prefetcher (long row segments): keeps a window of AHEAD quads of
+// X, V and (unless the pbest copy is pending) P in flight ahead of the
+// loads, crossing into the warp's next row.  Lane 0 issues; the cursor is
+// relative to the current row segment (c in [0, 2 seg)).
+struct WindowPrefetch {
+    const char* X;
+    const char* V;
+    const char* P;
+    long long ld_bytes, qb, seg, ahead;
+    long long row, nxt;  // current and next row of the warp (nxt >= rows: none)
+    bool pend_cur, pend_nxt, on;
+    long long c;         // next unprefetched quad, relative to qb of the current row
+    __device__ __forceinline__ void issue(long long r, long long q0, long long n, bool pend) {
+        const long long o = r * ld_bytes + (qb + q0) * 16;
+        prefetch_l2(X + o, n * 16);
+        prefetch_l2(V + o, n * 16);
+        if (!pend) prefetch_l2(P + o, n * 16);
+    }
+    __device__ __forceinline__ void operator()(long long base) {
+        if (!on) return;
+        long long target = (base - qb) + ahead;
+        const long long lim = nxt >= 0 ? 2 * seg : seg;
+        if (target > lim) target = lim;
+        if (c >= target) return;
+        if (c < seg) {
+            const long long e = target < seg ? target : seg;
+            issue(row, c, e - c, pend_cur);
+            c = e;
+        }
+        if (c < target) {  // into the next row
+            issue(nxt, c - seg, target - c, pend_nxt);
+            c = target;
+        }
+    }
+};
 
 // ---------------------------------------------------------------------------
-// Grid-level argmin + finalize (A12/A13).  Every thread calls it after its
-// last row; `my_key` is meaningful in any thread (~0 = none).
+// Grid-level argmin + finalize (A12/A13).
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long k) {
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) {
-        const unsigned long long o = __shfl_xor_sync(0xffffffffu, k, m);
+        const unsigned long long o = __shfl_xor_sync(FULL, k, m);
         k = o < k ? o : k;
     }
     return k;
 }
 
-// Returns true in the (whole) last CTA to finish; key in *out_key.
+// Every thread calls it after its last row; returns true in the (whole) last
+// CTA to finish, with the generation's min key in *out_key.
 __device__ __forceinline__ bool grid_argmin(Ctl* ctl, unsigned long long my_key,
                                             unsigned long long* out_key) {
     __shared__ unsigned long long sh_k[32];
@@ -258,8 +378,8 @@ __device__ __forceinline__ bool grid_argmin(Ctl* ctl, unsigned long long my_key,
     return true;
 }
 
-// In the last CTA: gbest update (strict, R-5), hist, record for world > 1.
-// `t_new` is the index of the population just evaluated.
+// In the last CTA: gbest update (strict, R-5), hist, or the winner record for
+// the exchange.  `t_new` is the index of the population just evaluated.
 __device__ void pso_finalize(const PsoArgs& a, unsigned long long key, unsigned long long t_new) {
     Ctl* ctl = a.ctl;
     const long long NQ = a.ld >> 2;
@@ -302,30 +422,34 @@ __device__ void pso_finalize(const PsoArgs& a, unsigned long long key, unsigned 
 // ---------------------------------------------------------------------------
 // Kernels
 
-// A2: X0 = fmaf(u, ub-lb, lb) (Philox tag 0, t = 0), V0 = 0, P0 = X0.
-__global__ void k_pso_init(PsoArgs a) {
-    const long long NQ = a.ld >> 2;
-    const long long total = a.rows * NQ;
+// A2: X0 = fmaf(u, ub-lb, lb) (Philox tag 0, t = 0), V0 = 0 (+ P0 = X0 for PSO).
+__device__ __forceinline__ void init_population(float* X, float* V, float* P, long long rows,
+                                                long long row0, long long D, long long ld,
+                                                const float* lb, const float* ub, float lb0,
+                                                float ub0, int uniform, const PhiloxKey& rk) {
+    const long long NQ = ld >> 2;
+    const long long total = rows * NQ;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
         const long long r = i / NQ, q = i - r * NQ;
-        const uint4 b = Philox::run(make_uint4((uint32_t)q, (uint32_t)(a.row0 + r), 0u, 0u), a.k0,
-                                    a.k1);
-        const float4 lo = bound4(a.lb, a.lb0, a.uniform_bounds, q);
-        const float4 hi = bound4(a.ub, a.ub0, a.uniform_bounds, q);
-        float4 x;
+        const uint4 b = Philox::run(make_uint4((uint32_t)q, (uint32_t)(row0 + r), 0u, 0u), rk);
+        const float4 lo = bound4(lb, lb0, uniform, q);
+        const float4 hi = bound4(ub, ub0, uniform, q);
+        float4 x, v = make_float4(0.f, 0.f, 0.f, 0.f);
         x.x = __fmaf_rn(u24(b.x), __fsub_rn(hi.x, lo.x), lo.x);
         x.y = __fmaf_rn(u24(b.y), __fsub_rn(hi.y, lo.y), lo.y);
         x.z = __fmaf_rn(u24(b.z), __fsub_rn(hi.z, lo.z), lo.z);
         x.w = __fmaf_rn(u24(b.w), __fsub_rn(hi.w, lo.w), lo.w);
-        const long long j0 = 4 * q;
-        if (j0 + 1 >= a.D) x.y = 0.f;
-        if (j0 + 2 >= a.D) x.z = 0.f;
-        if (j0 + 3 >= a.D) x.w = 0.f;
-        reinterpret_cast<float4*>(a.X)[i] = x;
-        reinterpret_cast<float4*>(a.P)[i] = x;
-        reinterpret_cast<float4*>(a.V)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        zero_pad(x, v, q, D);
+        reinterpret_cast<float4*>(X)[i] = x;
+        reinterpret_cast<float4*>(V)[i] = v;
+        if (P) reinterpret_cast<float4*>(P)[i] = x;
     }
+}
+
+__global__ void k_pso_init(PsoArgs a) {
+    init_population(a.X, a.V, a.P, a.rows, a.row0, a.D, a.ld, a.lb, a.ub, a.lb0, a.ub0,
+                    a.uniform_bounds, a.rk);
     for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < a.rows;
          r += (long long)gridDim.x * blockDim.x) {
         a.pf[r] = __int_as_float(0x7f800000);
@@ -335,69 +459,97 @@ __global__ void k_pso_init(PsoArgs a) {
 }
 
 // evox_eval: fit[r] = f(X[r]).
-template <int P, int WPR>
-__global__ void __launch_bounds__(WPR == 1 ? 256 : WPR * 32) k_eval(const float* __restrict__ X, long long rows,
-                                              long long D, long long ld, float* __restrict__ fit) {
-    __shared__ Fit<P> sh_acc[WPR > 1 ? WPR : 1];
-    __shared__ float sh_head[WPR > 1 ? WPR : 1];
-    constexpr int RPC = (WPR == 1) ? 8 : 1;  // rows per CTA pass
-    const int wid = threadIdx.x >> 5;
-    const int wr = (WPR == 1) ? 0 : wid;
-    const int slot = (WPR == 1) ? wid : 0;
-    long long qb, qe;
-    row_segment(ld >> 2, WPR, wr, qb, qe);
-    for (long long row = (long long)blockIdx.x * RPC + slot; row < rows;
-         row += (long long)gridDim.x * RPC) {
+template <int P, class G>
+__global__ void __launch_bounds__(256) k_eval(const float* __restrict__ X, long long rows,
+                                              long long D, long long ld,
+                                              float* __restrict__ fit) {
+    __shared__ Fit<P> sh_acc[G::WPR];
+    __shared__ float sh_head[G::WPR];
+    __shared__ __align__(16) HStore<P> sh_h;
+    const float* htab = HTable<P, G>::fill(sh_h.v, ld);
+    const RowMap<G> m(ld >> 2);
+    NoPrefetch pf;
+    for (long long it = 0;; ++it) {
+        const long long wrow = m.wfirst + it * m.stride;
+        if (wrow >= rows) break;  // warp-uniform (CTA-uniform for WPR > 1)
+        const long long row = m.first + it * m.stride;
+        const bool ok = row < rows;
         MoverEval mv;
-        mv.Xr = reinterpret_cast<const float4*>(X + row * ld);
+        mv.Xr = reinterpret_cast<const float4*>(X + (ok ? row : 0) * ld);
         Fit<P> acc;
         float hx, tx;
         bool tv;
-        walk_segment<P>(mv, qb, qe, D, acc, hx, tx, tv);
-        const float f = reduce_row<P, WPR>(acc, D, hx, tx, tv, sh_acc, sh_head);
-        if ((WPR == 1) ? (threadIdx.x & 31) == 0 : threadIdx.x == 0) fit[row] = f;
+        walk_segment<P, G>(mv, m.qb, m.qe, D, ok, acc, hx, tx, tv, pf, htab);
+        const float f = reduce_row<P, G>(acc, D, hx, tx, tv, sh_acc, sh_head);
+        if (m.leader && ok) fit[row] = f;
     }
 }
 
 // Fused PSO generation: lazy pbest + move + clip + evaluate + tell + argmin.
-template <int P, int WPR>
-__global__ void __launch_bounds__(WPR == 1 ? 256 : WPR * 32) k_pso_gen(PsoArgs a) {
-    __shared__ Fit<P> sh_acc[WPR > 1 ? WPR : 1];
-    __shared__ float sh_head[WPR > 1 ? WPR : 1];
-    constexpr int RPC = (WPR == 1) ? 8 : 1;
-    const int wid = threadIdx.x >> 5, lane = lane_id();
-    const int wr = (WPR == 1) ? 0 : wid;
-    const int slot = (WPR == 1) ? wid : 0;
+template <int P, class G>
+__global__ void __launch_bounds__(256, 2) k_pso_gen(PsoArgs a) {
+    __shared__ Fit<P> sh_acc[G::WPR];
+    __shared__ float sh_head[G::WPR];
+    __shared__ __align__(16) HStore<P> sh_h;
+    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+    const RowMap<G> m(a.ld >> 2);
+    const int lane = lane_id();
     const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
-    long long qb, qe;
-    row_segment(a.ld >> 2, WPR, wr, qb, qe);
+    const long long seg = m.qe - m.qb;
+    // prefetch mode: A = the warp's whole next rows (short rows), B = sliding window
+    const bool mode_a = seg * G::RPW <= MODE_A_MAX;
+    WindowPrefetch wp;
+    wp.X = reinterpret_cast<const char*>(a.X);
+    wp.V = reinterpret_cast<const char*>(a.V);
+    wp.P = reinterpret_cast<const char*>(a.P);
+    wp.ld_bytes = a.ld * 4;
+    wp.qb = m.qb;
+    wp.seg = seg;
+    wp.ahead = seg < 2 * G::GROUP ? seg : 2 * G::GROUP;
+    wp.on = !mode_a && lane == 0;
+    wp.c = 0;
     unsigned long long best = ~0ull;
-    const long long stride = (long long)gridDim.x * RPC;
-    const long long seg_off = qb * 16, seg_bytes = (qe - qb) * 16;
-    long long row = (long long)blockIdx.x * RPC + slot;
-    // pbest-pending flags one and two rows ahead (imp[r] is rewritten only by
-    // the warp(s) that own row r, later in this kernel, so these reads see the
-    // previous generation's decisions).
-    bool pend_cur = row < a.rows ? a.imp[row] != 0 : false;
-    bool pend_nxt = row + stride < a.rows ? a.imp[row + stride] != 0 : true;
-    for (; row < a.rows; row += stride) {
-        const long long nxt = row + stride, nn = nxt + stride;
-        if (lane == 0 && nxt < a.rows) {  // next row of this warp: HBM -> L2 now
-            const long long o = nxt * a.ld * 4 + seg_off;
-            prefetch_l2(reinterpret_cast<const char*>(a.X) + o, seg_bytes);
-            prefetch_l2(reinterpret_cast<const char*>(a.V) + o, seg_bytes);
-            if (!pend_nxt) prefetch_l2(reinterpret_cast<const char*>(a.P) + o, seg_bytes);
+    // pbest-pending flags one and two iterations ahead (imp[r] is rewritten only
+    // by the thread group that owns row r, later in this kernel, so these reads
+    // see the previous generation's decisions).
+    long long row = m.first;
+    bool pend_cur = row < a.rows ? a.imp[row] != 0 : true;
+    bool pend_nxt = row + m.stride < a.rows ? a.imp[row + m.stride] != 0 : true;
+    for (long long it = 0;; ++it, row += m.stride) {
+        const long long wrow = m.wfirst + it * m.stride;
+        if (wrow >= a.rows) break;  // warp-uniform (CTA-uniform for WPR > 1)
+        const bool ok = row < a.rows;
+        const long long nxt = row + m.stride, nn = nxt + m.stride;
+        const bool nxt_ok = nxt < a.rows;
+        if (mode_a) {
+            // the warp's next rows, HBM -> L2 now (X, V contiguous; P per row unless pending)
+            const long long wn = wrow + m.stride;
+            if (lane == 0 && wn < a.rows) {
+                long long nr = a.rows - wn < G::RPW ? a.rows - wn : G::RPW;
+                const long long o = wn * a.ld * 4 + m.qb * 16;
+                const long long bytes = G::WPR == 1 ? nr * a.ld * 4 : seg * 16;
+                prefetch_l2(reinterpret_cast<const char*>(a.X) + o, bytes);
+                prefetch_l2(reinterpret_cast<const char*>(a.V) + o, bytes);
+            }
+            if (m.sl == 0 && nxt_ok && !pend_nxt)
+                prefetch_l2(reinterpret_cast<const char*>(a.P) + nxt * a.ld * 4 + m.qb * 16,
+                            seg * 16);
+        } else {
+            wp.row = row;
+            wp.nxt = nxt_ok ? nxt : -1;
+            wp.pend_cur = pend_cur;
+            wp.pend_nxt = pend_nxt;
         }
         const bool pend_nn = nn < a.rows ? a.imp[nn] != 0 : true;
         float pf_old = 0.0f;
-        if (lane == 0) pf_old = a.pf[row];
-        MoverPso mv(a, row, (uint32_t)t, pend_cur);
+        if (m.leader && ok) pf_old = a.pf[row];
+        MoverPso mv(a, ok ? row : 0, (uint32_t)t, pend_cur);
         Fit<P> acc;
         float hx, tx;
         bool tv;
-        walk_segment<P>(mv, qb, qe, a.D, acc, hx, tx, tv);
-        const float f = reduce_row<P, WPR>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
-        if (lane == 0 && (WPR == 1 || wid == 0)) {
+        walk_segment<P, G>(mv, m.qb, m.qe, a.D, ok, acc, hx, tx, tv, wp, htab);
+        const float f = reduce_row<P, G>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
+        if (m.leader && ok) {
             // per-row tell (A11): strict improvement, NaN never improves
             const bool imp = f < pf_old;
             a.f[row] = f;
@@ -408,31 +560,35 @@ __global__ void __launch_bounds__(WPR == 1 ? 256 : WPR * 32) k_pso_gen(PsoArgs a
         }
         pend_cur = pend_nxt;
         pend_nxt = pend_nn;
+        wp.c = wp.c > seg ? wp.c - seg : 0;
     }
     unsigned long long key;
     if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
 }
 
 // Unfused ask: move X_t -> X_{t+1} (no evaluation).
-template <int WPR>
-__global__ void __launch_bounds__(WPR == 1 ? 256 : WPR * 32) k_pso_move(PsoArgs a,
-                                                                        unsigned long long t) {
-    constexpr int RPC = (WPR == 1) ? 8 : 1;
-    const int wid = threadIdx.x >> 5;
-    const int wr = (WPR == 1) ? 0 : wid;
-    const int slot = (WPR == 1) ? wid : 0;
-    long long qb, qe;
-    row_segment(a.ld >> 2, WPR, wr, qb, qe);
-    for (long long row = (long long)blockIdx.x * RPC + slot; row < a.rows;
-         row += (long long)gridDim.x * RPC) {
-        MoverPso mv(a, row, (uint32_t)t, a.imp[row] != 0);
+template <class G>
+__global__ void __launch_bounds__(256) k_pso_move(PsoArgs a, unsigned long long t) {
+    __shared__ Fit<SPHERE> sh_acc[G::WPR];
+    __shared__ float sh_head[G::WPR];
+    (void)sh_acc;
+    (void)sh_head;
+    const RowMap<G> m(a.ld >> 2);
+    NoPrefetch pf;
+    for (long long it = 0;; ++it) {
+        const long long wrow = m.wfirst + it * m.stride;
+        if (wrow >= a.rows) break;
+        const long long row = m.first + it * m.stride;
+        const bool ok = row < a.rows;
+        const bool pend = ok ? a.imp[row] != 0 : false;
+        MoverPso mv(a, ok ? row : 0, (uint32_t)t, pend);
         Fit<SPHERE> acc;  // unused
         float hx, tx;
         bool tv;
-        walk_segment<SPHERE>(mv, qb, qe, a.D, acc, hx, tx, tv);
+        walk_segment<SPHERE, G>(mv, m.qb, m.qe, a.D, ok, acc, hx, tx, tv, pf);
         __syncwarp();
-        if (WPR > 1) __syncthreads();
-        if (lane_id() == 0 && (WPR == 1 || wid == 0)) a.imp[row] = 0;
+        if constexpr (G::WPR > 1) __syncthreads();
+        if (m.leader && ok) a.imp[row] = 0;
     }
 }
 
@@ -496,8 +652,8 @@ __global__ void __launch_bounds__(256) k_gbest_select(PsoArgs a) {
 __global__ void __launch_bounds__(256) k_pso_materialize(PsoArgs a) {
     const long long NQ = a.ld >> 2;
     const int wid = threadIdx.x >> 5, lane = lane_id();
-    for (long long row = (long long)blockIdx.x * 8 + wid; row < a.rows;
-         row += (long long)gridDim.x * 8) {
+    for (long long row = (long long)blockIdx.x * WARPS + wid; row < a.rows;
+         row += (long long)gridDim.x * WARPS) {
         if (!a.imp[row]) continue;
         const float4* x = reinterpret_cast<const float4*>(a.X + row * a.ld);
         float4* p = reinterpret_cast<float4*>(a.P + row * a.ld);
@@ -507,7 +663,6 @@ __global__ void __launch_bounds__(256) k_pso_materialize(PsoArgs a) {
     }
 }
 
-
 // ---------------------------------------------------------------------------
 // CSO (Table II; R-8)
 
@@ -515,10 +670,10 @@ __global__ void __launch_bounds__(256) k_pso_materialize(PsoArgs a) {
 struct CsoPerm {
     uint32_t k[4];
     uint32_t h, mask, Bb;
-    __device__ __forceinline__ void init(uint32_t blk, uint32_t t, uint32_t Bb_, uint32_t k0,
-                                         uint32_t k1) {
-        const uint4 rk = Philox::run(make_uint4(blk, 0u, t, 4u), k0, k1);
-        k[0] = rk.x; k[1] = rk.y; k[2] = rk.z; k[3] = rk.w;
+    __device__ __forceinline__ void init(uint32_t blk, uint32_t t, uint32_t Bb_,
+                                         const PhiloxKey& rk) {
+        const uint4 r = Philox::run(make_uint4(blk, 0u, t, 4u), rk);
+        k[0] = r.x; k[1] = r.y; k[2] = r.z; k[3] = r.w;
         Bb = Bb_;
         uint32_t b = 0;
         while (b < 32 && (1ull << b) < (unsigned long long)Bb) ++b;
@@ -547,18 +702,13 @@ struct CsoPerm {
 
 // Loser update of one row (A15): v = fmaf(R2, xw-xl, R1*vl) [+ phi R3 (xbar-xl)], clip.
 struct MoverCso {
+    const CsoArgs& a;
     float4* Xl;
     float4* Vl;
     const float4* Xw;
-    const float4* lb;
-    const float4* ub;
-    const float4* xbar;
-    float lb0, ub0, phi;
-    const PhiloxKey* rk;
     uint32_t row_g, t;
-    bool uni;
-    long long D;
     float4 x[U], v[U], xw[U];
+    __device__ __forceinline__ MoverCso(const CsoArgs& a_) : a(a_) {}
     __device__ __forceinline__ void load(int u, long long q) {
         x[u] = ld_stream(Xl + q);
         v[u] = ld_stream(Vl + q);
@@ -573,29 +723,25 @@ struct MoverCso {
         return clipf(__fadd_rn(xl, v), lo, hi);
     }
     __device__ __forceinline__ float4 step(int u, long long q) {
-        const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 5u), *rk);
-        const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 6u), *rk);
-        const bool use3 = phi != 0.0f;
+        const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 5u), a.rk);
+        const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 6u), a.rk);
+        const bool use3 = a.phi != 0.0f;
         float4 c3 = make_float4(0.f, 0.f, 0.f, 0.f), xb = c3;
         if (use3) {
-            const uint4 b3 = Philox::run(make_uint4((uint32_t)q, row_g, t, 7u), *rk);
+            const uint4 b3 = Philox::run(make_uint4((uint32_t)q, row_g, t, 7u), a.rk);
+            const float phi = a.phi;
             c3 = make_float4(__fmul_rn(phi, u24(b3.x)), __fmul_rn(phi, u24(b3.y)),
                              __fmul_rn(phi, u24(b3.z)), __fmul_rn(phi, u24(b3.w)));
-            xb = __ldg(xbar + q);
+            xb = __ldg(reinterpret_cast<const float4*>(a.xbar) + q);
         }
-        const float4 lo = uni ? make_float4(lb0, lb0, lb0, lb0) : __ldg(lb + q);
-        const float4 hi = uni ? make_float4(ub0, ub0, ub0, ub0) : __ldg(ub + q);
+        const float4 lo = bound4(a.lb, a.lb0, a.uniform_bounds, q);
+        const float4 hi = bound4(a.ub, a.ub0, a.uniform_bounds, q);
         float4 xn, vn;
         xn.x = upd(x[u].x, v[u].x, xw[u].x, u24(b1.x), u24(b2.x), c3.x, xb.x, use3, lo.x, hi.x, vn.x);
         xn.y = upd(x[u].y, v[u].y, xw[u].y, u24(b1.y), u24(b2.y), c3.y, xb.y, use3, lo.y, hi.y, vn.y);
         xn.z = upd(x[u].z, v[u].z, xw[u].z, u24(b1.z), u24(b2.z), c3.z, xb.z, use3, lo.z, hi.z, vn.z);
         xn.w = upd(x[u].w, v[u].w, xw[u].w, u24(b1.w), u24(b2.w), c3.w, xb.w, use3, lo.w, hi.w, vn.w);
-        if (4 * q + 3 >= D) {
-            const long long j0 = 4 * q;
-            if (j0 + 1 >= D) { xn.y = 0.f; vn.y = 0.f; }
-            if (j0 + 2 >= D) { xn.z = 0.f; vn.z = 0.f; }
-            if (j0 + 3 >= D) { xn.w = 0.f; vn.w = 0.f; }
-        }
+        zero_pad(xn, vn, q, a.D);
         st_stream(Xl + q, xn);
         st_stream(Vl + q, vn);
         return xn;
@@ -617,72 +763,90 @@ __device__ void cso_finalize(const CsoArgs& a, unsigned long long key, unsigned 
     }
 }
 
+// The pair (or the unpaired odd member) of CSO work item `it` (R-8).
+struct CsoItem {
+    long long gw, gl;  // winner, loser global rows (gl < 0: unpaired member gw passes)
+    float fw;
+    bool valid;
+};
+
+__device__ __forceinline__ CsoItem cso_item(const CsoArgs& a, long long it, uint32_t t) {
+    CsoItem r;
+    r.valid = false;
+    r.gl = -1;
+    r.gw = 0;
+    r.fw = 0.f;
+    const long long blk0 = a.row0 / a.B;
+    const long long ipb = (a.B + 1) / 2;
+    const long long bl = it / ipb, p = it - bl * ipb;
+    const long long blk = blk0 + bl;
+    const long long base = blk * a.B;
+    if (base >= a.pop) return r;
+    const long long Bb = (base + a.B <= a.pop) ? a.B : a.pop - base;
+    if (p >= (Bb + 1) / 2) return r;
+    CsoPerm perm;
+    perm.init((uint32_t)blk, t, (uint32_t)Bb, a.rk);
+    r.valid = true;
+    if (2 * p + 1 >= Bb) {  // odd block: unpaired member passes unchanged
+        r.gw = base + perm((uint32_t)(Bb - 1));
+        r.fw = a.f[r.gw - a.row0];
+        return r;
+    }
+    const long long gi = base + perm((uint32_t)(2 * p));
+    const long long gk = base + perm((uint32_t)(2 * p + 1));
+    const float fi = a.f[gi - a.row0], fk = a.f[gk - a.row0];
+    const float oi = fi != fi ? __int_as_float(0x7f800000) : fi;
+    const float ok = fk != fk ? __int_as_float(0x7f800000) : fk;
+    const bool i_wins = oi < ok || (oi == ok && gi < gk);
+    r.gw = i_wins ? gi : gk;
+    r.gl = i_wins ? gk : gi;
+    r.fw = i_wins ? fi : fk;
+    return r;
+}
+
 // One CSO generation over this shard's whole blocks.  One work item per pair
-// (plus one for the unpaired member of an odd block); WPR warps per item.
-template <int P, int WPR>
-__global__ void __launch_bounds__(WPR == 1 ? 256 : WPR * 32) k_cso_gen(CsoArgs a) {
-    __shared__ Fit<P> sh_acc[WPR > 1 ? WPR : 1];
-    __shared__ float sh_head[WPR > 1 ? WPR : 1];
-    constexpr int RPC = (WPR == 1) ? 8 : 1;
-    const int wid = threadIdx.x >> 5, lane = lane_id();
-    const int wr = (WPR == 1) ? 0 : wid;
-    const int slot = (WPR == 1) ? wid : 0;
+// (plus one for the unpaired member of an odd block), mapped like a row.
+template <int P, class G>
+__global__ void __launch_bounds__(256, 2) k_cso_gen(CsoArgs a) {
+    __shared__ Fit<P> sh_acc[G::WPR];
+    __shared__ float sh_head[G::WPR];
+    __shared__ __align__(16) HStore<P> sh_h;
+    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+    const RowMap<G> m(a.ld >> 2);
     const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
-    long long qb, qe;
-    row_segment(a.ld >> 2, WPR, wr, qb, qe);
     const long long blk0 = a.row0 / a.B;
     const long long nblk = (a.row0 + a.rows + a.B - 1) / a.B - blk0;
-    const long long ipb = (a.B + 1) / 2;
-    const long long items = nblk * ipb;
+    const long long items = nblk * ((a.B + 1) / 2);
+    NoPrefetch pf;
     unsigned long long best = ~0ull;
-    for (long long it = (long long)blockIdx.x * RPC + slot; it < items;
-         it += (long long)gridDim.x * RPC) {
-        const long long bl = it / ipb, p = it - bl * ipb;
-        const long long blk = blk0 + bl;
-        const long long base = blk * a.B;
-        const long long Bb = (base + a.B <= a.pop) ? a.B : a.pop - base;
-        if (p >= (Bb + 1) / 2) continue;  // uniform across the item's warps
-        CsoPerm perm;
-        perm.init((uint32_t)blk, (uint32_t)t, (uint32_t)Bb, a.k0, a.k1);
-        if (2 * p + 1 >= Bb) {  // odd block: unpaired member passes unchanged
-            const long long gi = base + perm((uint32_t)(Bb - 1));
-            if (lane == 0 && (WPR == 1 || wid == 0)) {
-                const unsigned long long k = make_key(a.f[gi - a.row0], gi);
-                best = k < best ? k : best;
-            }
-            continue;
-        }
-        const long long gi = base + perm((uint32_t)(2 * p));
-        const long long gk = base + perm((uint32_t)(2 * p + 1));
-        float fi = a.f[gi - a.row0], fk = a.f[gk - a.row0];
-        const float oi = fi != fi ? __int_as_float(0x7f800000) : fi;
-        const float ok = fk != fk ? __int_as_float(0x7f800000) : fk;
-        const bool i_wins = oi < ok || (oi == ok && gi < gk);
-        const long long gw = i_wins ? gi : gk, gl = i_wins ? gk : gi;
-        const float fw = i_wins ? fi : fk;
-        MoverCso mv;
-        mv.Xl = reinterpret_cast<float4*>(a.X + (gl - a.row0) * a.ld);
-        mv.Vl = reinterpret_cast<float4*>(a.V + (gl - a.row0) * a.ld);
-        mv.Xw = reinterpret_cast<const float4*>(a.X + (gw - a.row0) * a.ld);
-        mv.lb = reinterpret_cast<const float4*>(a.lb);
-        mv.ub = reinterpret_cast<const float4*>(a.ub);
-        mv.xbar = reinterpret_cast<const float4*>(a.xbar);
-        mv.lb0 = a.lb0; mv.ub0 = a.ub0; mv.phi = a.phi;
-        mv.rk = &a.rk;
-        mv.row_g = (uint32_t)gl;
+    for (long long k = 0;; ++k) {
+        const long long witem = m.wfirst + k * m.stride;
+        if (witem >= items) break;
+        const long long it = m.first + k * m.stride;
+        CsoItem ci;
+        ci.valid = false;
+        if (it < items) ci = cso_item(a, it, (uint32_t)t);
+        const bool pair = ci.valid && ci.gl >= 0;
+        MoverCso mv(a);
+        const long long lrow = pair ? ci.gl - a.row0 : 0, wrow = pair ? ci.gw - a.row0 : 0;
+        mv.Xl = reinterpret_cast<float4*>(a.X + lrow * a.ld);
+        mv.Vl = reinterpret_cast<float4*>(a.V + lrow * a.ld);
+        mv.Xw = reinterpret_cast<const float4*>(a.X + wrow * a.ld);
+        mv.row_g = (uint32_t)(pair ? ci.gl : 0);
         mv.t = (uint32_t)t;
-        mv.uni = a.uniform_bounds != 0;
-        mv.D = a.D;
         Fit<P> acc;
         float hx, tx;
         bool tv;
-        walk_segment<P>(mv, qb, qe, a.D, acc, hx, tx, tv);
-        const float fl = reduce_row<P, WPR>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
-        if (lane == 0 && (WPR == 1 || wid == 0)) {
-            a.f[gl - a.row0] = fl;
-            const unsigned long long kw = make_key(fw, gw), kl = make_key(fl, gl);
-            const unsigned long long k = kw < kl ? kw : kl;
-            best = k < best ? k : best;
+        walk_segment<P, G>(mv, m.qb, m.qe, a.D, pair, acc, hx, tx, tv, pf, htab);
+        const float fl = reduce_row<P, G>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
+        if (m.leader && ci.valid) {
+            unsigned long long kk = make_key(ci.fw, ci.gw);
+            if (pair) {
+                a.f[ci.gl - a.row0] = fl;
+                const unsigned long long kl = make_key(fl, ci.gl);
+                kk = kl < kk ? kl : kk;
+            }
+            best = kk < best ? kk : best;
         }
     }
     unsigned long long key;
@@ -701,29 +865,9 @@ __global__ void __launch_bounds__(256) k_cso_tell0(CsoArgs a) {
     if (grid_argmin(a.ctl, best, &key)) cso_finalize(a, key, 0);
 }
 
-// CSO init: X0 = fmaf(u, ub-lb, lb) (tag 0, t = 0), V0 = 0 -- same stream as PSO init.
 __global__ void k_cso_init(CsoArgs a) {
-    const long long NQ = a.ld >> 2;
-    const long long total = a.rows * NQ;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long r = i / NQ, q = i - r * NQ;
-        const uint4 b = Philox::run(make_uint4((uint32_t)q, (uint32_t)(a.row0 + r), 0u, 0u), a.k0,
-                                    a.k1);
-        const float4 lo = bound4(a.lb, a.lb0, a.uniform_bounds, q);
-        const float4 hi = bound4(a.ub, a.ub0, a.uniform_bounds, q);
-        float4 x;
-        x.x = __fmaf_rn(u24(b.x), __fsub_rn(hi.x, lo.x), lo.x);
-        x.y = __fmaf_rn(u24(b.y), __fsub_rn(hi.y, lo.y), lo.y);
-        x.z = __fmaf_rn(u24(b.z), __fsub_rn(hi.z, lo.z), lo.z);
-        x.w = __fmaf_rn(u24(b.w), __fsub_rn(hi.w, lo.w), lo.w);
-        const long long j0 = 4 * q;
-        if (j0 + 1 >= a.D) x.y = 0.f;
-        if (j0 + 2 >= a.D) x.z = 0.f;
-        if (j0 + 3 >= a.D) x.w = 0.f;
-        reinterpret_cast<float4*>(a.X)[i] = x;
-        reinterpret_cast<float4*>(a.V)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    init_population(a.X, a.V, nullptr, a.rows, a.row0, a.D, a.ld, a.lb, a.ub, a.lb0, a.ub0,
+                    a.uniform_bounds, a.rk);
 }
 
 // Column means for the phi != 0 term: fixed row chunks of 1024, fp64 partial
@@ -776,11 +920,10 @@ __global__ void __launch_bounds__(1024) k_argmin_rows(const float* f, long long 
     }
 }
 
-__global__ void k_debug_philox(const uint4* ctr, uint32_t k0, uint32_t k1, uint4* out,
-                               long long n) {
+__global__ void k_debug_philox(const uint4* ctr, PhiloxKey rk, uint4* out, long long n) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
-        out[i] = Philox::run(ctr[i], k0, k1);
+        out[i] = Philox::run(ctr[i], rk);
 }
 
 // ----------------------------------------------------------------- dispatch
@@ -790,62 +933,78 @@ int sm_count(int device) {
     return n;
 }
 
-}  // namespace
+using G8 = Geom<8, 1>;
+using G32 = Geom<32, 1>;
+using GW8 = Geom<32, 8>;
 
-int wpr_for_dim(long long ld) {
+// 0: 8 lanes per row (ld <= 256), 1: a warp per row (ld <= 4096), 2: a CTA per row.
+int geom_id(long long ld) {
     const long long NQ = ld >> 2;
+    if (NQ <= 64) return 0;
     if (NQ <= 1024) return 1;
-    if (NQ <= 8192) return 8;
-    return 32;
+    return 2;
 }
 
-#define EVOX_DISPATCH_WPR(wpr, ...)          \
-    do {                                      \
-        if ((wpr) == 1) {                     \
-            constexpr int W_ = 1;             \
-            __VA_ARGS__;                             \
-        } else if ((wpr) == 8) {              \
-            constexpr int W_ = 8;             \
-            __VA_ARGS__;                             \
-        } else {                              \
-            constexpr int W_ = 32;            \
-            __VA_ARGS__;                             \
-        }                                     \
-    } while (0)
-
-#define EVOX_DISPATCH_PROB(p, ...)            \
-    do {                                       \
-        switch (p) {                           \
-            case SPHERE: {                     \
-                constexpr int P_ = SPHERE;     \
-                __VA_ARGS__;                          \
-            } break;                           \
-            case ACKLEY: {                     \
-                constexpr int P_ = ACKLEY;     \
-                __VA_ARGS__;                          \
-            } break;                           \
-            case RASTRIGIN: {                  \
-                constexpr int P_ = RASTRIGIN;  \
-                __VA_ARGS__;                          \
-            } break;                           \
-            case GRIEWANK: {                   \
-                constexpr int P_ = GRIEWANK;   \
-                __VA_ARGS__;                          \
-            } break;                           \
-            default: {                         \
-                constexpr int P_ = ROSENBROCK; \
-                __VA_ARGS__;                          \
-            } break;                           \
-        }                                      \
-    } while (0)
-
-static int grid_for(const void* fn, int threads, long long units, int device) {
+int grid_for(const void* fn, long long units, int device) {
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
     if (per_sm < 1) per_sm = 1;
     long long g = (long long)sm_count(device) * per_sm;
     if (units < g) g = units;
     return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+int wpr_for_dim(long long ld) { return geom_id(ld) == 2 ? 8 : 1; }
+
+#define EVOX_DISPATCH_GEOM(ld, ...)     \
+    do {                                \
+        switch (geom_id(ld)) {          \
+            case 0: {                   \
+                using G_ = G8;          \
+                __VA_ARGS__;            \
+            } break;                    \
+            case 1: {                   \
+                using G_ = G32;         \
+                __VA_ARGS__;            \
+            } break;                    \
+            default: {                  \
+                using G_ = GW8;         \
+                __VA_ARGS__;            \
+            } break;                    \
+        }                               \
+    } while (0)
+
+#define EVOX_DISPATCH_PROB(p, ...)             \
+    do {                                       \
+        switch (p) {                           \
+            case SPHERE: {                     \
+                constexpr int P_ = SPHERE;     \
+                __VA_ARGS__;                   \
+            } break;                           \
+            case ACKLEY: {                     \
+                constexpr int P_ = ACKLEY;     \
+                __VA_ARGS__;                   \
+            } break;                           \
+            case RASTRIGIN: {                  \
+                constexpr int P_ = RASTRIGIN;  \
+                __VA_ARGS__;                   \
+            } break;                           \
+            case GRIEWANK: {                   \
+                constexpr int P_ = GRIEWANK;   \
+                __VA_ARGS__;                   \
+            } break;                           \
+            default: {                         \
+                constexpr int P_ = ROSENBROCK; \
+                __VA_ARGS__;                   \
+            } break;                           \
+        }                                      \
+    } while (0)
+
+template <class G>
+static long long row_units(long long rows) {
+    return (rows + G::RPC - 1) / G::RPC;
 }
 
 cudaError_t launch_pso_init(const PsoArgs& a, cudaStream_t st) {
@@ -862,32 +1021,24 @@ cudaError_t launch_eval(int problem, const float* X, long long rows, long long D
     if (rows <= 0) return cudaSuccess;
     int dev = 0;
     cudaGetDevice(&dev);
-    const int wpr = wpr_for_dim(ld);
-    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_WPR(wpr, {
-        const int threads = W_ == 1 ? 256 : W_ * 32;
-        const long long units = W_ == 1 ? (rows + 7) / 8 : rows;
-        const int g = grid_for((const void*)k_eval<P_, W_>, threads, units, dev);
-        k_eval<P_, W_><<<g, threads, 0, st>>>(X, rows, D, ld, fit);
+    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
+        const int g = grid_for((const void*)k_eval<P_, G_>, row_units<G_>(rows), dev);
+        k_eval<P_, G_><<<g, 256, 0, st>>>(X, rows, D, ld, fit);
     }));
     return cudaGetLastError();
 }
 
 int pso_gen_grid(int problem, long long ld, long long rows, int device) {
-    const int wpr = wpr_for_dim(ld);
     int g = 1;
-    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_WPR(wpr, {
-        const int threads = W_ == 1 ? 256 : W_ * 32;
-        const long long units = W_ == 1 ? (rows + 7) / 8 : rows;
-        g = grid_for((const void*)k_pso_gen<P_, W_>, threads, units, device);
+    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
+        g = grid_for((const void*)k_pso_gen<P_, G_>, row_units<G_>(rows), device);
     }));
     return g;
 }
 
 cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st) {
-    const int wpr = wpr_for_dim(a.ld);
-    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_WPR(wpr, {
-        const int threads = W_ == 1 ? 256 : W_ * 32;
-        k_pso_gen<P_, W_><<<grid, threads, 0, st>>>(a);
+    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+        k_pso_gen<P_, G_><<<grid, 256, 0, st>>>(a);
     }));
     return cudaGetLastError();
 }
@@ -895,12 +1046,9 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
 cudaError_t launch_pso_move(const PsoArgs& a, unsigned long long t, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
-    const int wpr = wpr_for_dim(a.ld);
-    EVOX_DISPATCH_WPR(wpr, {
-        const int threads = W_ == 1 ? 256 : W_ * 32;
-        const long long units = W_ == 1 ? (a.rows + 7) / 8 : a.rows;
-        const int g = grid_for((const void*)k_pso_move<W_>, threads, units, dev);
-        k_pso_move<W_><<<g, threads, 0, st>>>(a, t);
+    EVOX_DISPATCH_GEOM(a.ld, {
+        const int g = grid_for((const void*)k_pso_move<G_>, row_units<G_>(a.rows), dev);
+        k_pso_move<G_><<<g, 256, 0, st>>>(a, t);
     });
     return cudaGetLastError();
 }
@@ -909,7 +1057,7 @@ cudaError_t launch_pso_tell(const PsoArgs& a, const float* fit, unsigned long lo
                             cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
-    const int g = grid_for((const void*)k_pso_tell, 256, (a.rows + 255) / 256, dev);
+    const int g = grid_for((const void*)k_pso_tell, (a.rows + 255) / 256, dev);
     k_pso_tell<<<g, 256, 0, st>>>(a, fit, t);
     return cudaGetLastError();
 }
@@ -920,7 +1068,7 @@ cudaError_t launch_gbest_select(const PsoArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_pso_materialize(const PsoArgs& a, cudaStream_t st) {
-    long long g = (a.rows + 7) / 8;
+    long long g = (a.rows + WARPS - 1) / WARPS;
     if (g > 148 * 8) g = 148 * 8;
     if (g < 1) g = 1;
     k_pso_materialize<<<(int)g, 256, 0, st>>>(a);
@@ -939,7 +1087,7 @@ cudaError_t launch_cso_init(const CsoArgs& a, cudaStream_t st) {
 cudaError_t launch_cso_tell0(const CsoArgs& a, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
-    const int g = grid_for((const void*)k_cso_tell0, 256, (a.rows + 255) / 256, dev);
+    const int g = grid_for((const void*)k_cso_tell0, (a.rows + 255) / 256, dev);
     k_cso_tell0<<<g, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
@@ -951,22 +1099,16 @@ static long long cso_items(const CsoArgs& a) {
 }
 
 int cso_gen_grid(int problem, const CsoArgs& a, int device) {
-    const int wpr = wpr_for_dim(a.ld);
-    const long long items = cso_items(a);
     int g = 1;
-    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_WPR(wpr, {
-        const int threads = W_ == 1 ? 256 : W_ * 32;
-        const long long units = W_ == 1 ? (items + 7) / 8 : items;
-        g = grid_for((const void*)k_cso_gen<P_, W_>, threads, units, device);
+    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+        g = grid_for((const void*)k_cso_gen<P_, G_>, row_units<G_>(cso_items(a)), device);
     }));
     return g;
 }
 
 cudaError_t launch_cso_gen(int problem, const CsoArgs& a, int grid, cudaStream_t st) {
-    const int wpr = wpr_for_dim(a.ld);
-    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_WPR(wpr, {
-        const int threads = W_ == 1 ? 256 : W_ * 32;
-        k_cso_gen<P_, W_><<<grid, threads, 0, st>>>(a);
+    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+        k_cso_gen<P_, G_><<<grid, 256, 0, st>>>(a);
     }));
     return cudaGetLastError();
 }
@@ -998,7 +1140,8 @@ cudaError_t launch_debug_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, u
     if (n <= 0) return cudaSuccess;
     long long g = (n + 255) / 256;
     if (g > 4096) g = 4096;
-    k_debug_philox<<<(int)g, 256, 0, st>>>(reinterpret_cast<const uint4*>(ctr), k0, k1,
+    const PhiloxKey rk = Philox::schedule(((uint64_t)k1 << 32) | k0);
+    k_debug_philox<<<(int)g, 256, 0, st>>>(reinterpret_cast<const uint4*>(ctr), rk,
                                            reinterpret_cast<uint4*>(out), n);
     return cudaGetLastError();
 }

@@ -65,8 +65,8 @@ def test_init_bitwise(N, D):
 
 
 # -------------------------------------------------------------------- eval
-EVAL_SHAPES = [(1, 1), (3, 2), (5, 3), (64, 4), (100, 10), (37, 33), (513, 1000), (16, 1001),
-               (8, 4099), (3, 40001), (2, 100000)]
+EVAL_SHAPES = [(1, 1), (3, 2), (5, 3), (64, 4), (100, 10), (37, 33), (130, 100), (9, 257),
+               (513, 1000), (16, 1001), (7, 3000), (8, 4099), (3, 40001), (2, 100000)]
 
 
 @pytest.mark.parametrize("problem", list(WL.BOUNDS))
@@ -111,6 +111,8 @@ PSO_CASES = [("sphere", 100, 10, -5.12, 5.12, 0),        # C1
              ("griewank", 40, 100, -600, 600, 3),
              ("rosenbrock", 33, 101, -5, 10, 4),
              ("rosenbrock", 9, 4099, -5, 10, 5),
+             ("griewank", 21, 3000, -600, 600, 7),
+             ("rosenbrock", 13, 2999, -5, 10, 8),
              ("ackley", 6, 40001, -32.768, 32.768, 6)]
 
 
