@@ -76,13 +76,15 @@ struct Base {
     // kernel timing (evox_*_set_timing)
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
+    std::vector<int64_t> ev_gens;
     double kernel_ms = 0.0;
     int64_t kernel_n = 0;
 };
 
-// Timed launch: events around the kernel enqueued by `launch`.
+// Timed launch: events around the kernel enqueued by `launch`, which runs
+// `gens` generations.
 template <class F>
-cudaError_t timed(Base* b, F launch) {
+cudaError_t timed(Base* b, F launch, int64_t gens = 1) {
     if (!b->timing) return launch();
     std::pair<cudaEvent_t, cudaEvent_t> ev;
     if (!b->ev_free.empty()) {
@@ -97,20 +99,23 @@ cudaError_t timed(Base* b, F launch) {
     if (e == cudaSuccess) e = launch();
     if (e == cudaSuccess) e = cudaEventRecord(ev.second, b->stream);
     b->ev_pending.push_back(ev);
+    b->ev_gens.push_back(gens);
     return e;
 }
 
 // After a stream sync: fold pending event pairs into the totals.
 cudaError_t collect_timing(Base* b) {
-    for (auto& ev : b->ev_pending) {
+    for (size_t i = 0; i < b->ev_pending.size(); ++i) {
+        auto& ev = b->ev_pending[i];
         float ms = 0.0f;
         cudaError_t e = cudaEventElapsedTime(&ms, ev.first, ev.second);
         if (e != cudaSuccess) return e;
         b->kernel_ms += ms;
-        b->kernel_n += 1;
+        b->kernel_n += b->ev_gens[i];
         b->ev_free.push_back(ev);
     }
     b->ev_pending.clear();
+    b->ev_gens.clear();
     return cudaSuccess;
 }
 
@@ -286,6 +291,7 @@ void base_release(Base* b) {
     for (auto& ev : b->ev_free) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
     b->ev_pending.clear();
     b->ev_free.clear();
+    b->ev_gens.clear();
     for (auto& kv : b->graphs) cudaGraphExecDestroy(kv.second);
     b->graphs.clear();
     if (b->comm) {
@@ -366,7 +372,7 @@ constexpr int64_t kChunk = 32;
 
 template <class F>
 evox_status run_graphed(Base* b, int problem, int64_t n, F one) {
-    static const bool no_graph = std::getenv("EVOX_NO_GRAPH") != nullptr;
+    const bool no_graph = std::getenv("EVOX_NO_GRAPH") != nullptr;
     if (no_graph || b->timing) {
         for (int64_t i = 0; i < n; ++i) {
             evox_status st = one();
@@ -620,6 +626,13 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
     if (n_gens == 0) return EVOX_OK;
     const PsoArgs a = s->args();
     const int grid = s->gen_grid[problem];
+    const bool no_small = std::getenv("EVOX_NO_SMALL") != nullptr;  // testing: force multi-CTA
+    if (!s->comm && !no_small && evox::pso_small(s->rows, s->ld)) {
+        CU(s, timed(s, [&] { return evox::launch_pso_run_small((int)problem, a, n_gens, s->stream); },
+                    n_gens));
+        s->t += n_gens;
+        return EVOX_OK;
+    }
     st = run_graphed(s, (int)problem, n_gens, [&]() -> evox_status {
         CU(s, timed(s, [&] { return evox::launch_pso_gen((int)problem, a, grid, s->stream); }));
         return pso_exchange(s);

@@ -84,6 +84,9 @@ cudaError_t launch_pso_tell(const PsoArgs& a, const float* fit, unsigned long lo
 cudaError_t launch_gbest_select(const PsoArgs& a, cudaStream_t st);
 cudaError_t launch_pso_materialize(const PsoArgs& a, cudaStream_t st);
 int pso_gen_grid(int problem, long long ld, long long rows, int device);
+// Tiny populations: all generations in one single-CTA launch (bitwise identical).
+bool pso_small(long long rows, long long ld);
+cudaError_t launch_pso_run_small(int problem, const PsoArgs& a, long long n, cudaStream_t st);
 
 cudaError_t launch_cso_init(const CsoArgs& a, cudaStream_t st);
 cudaError_t launch_cso_tell0(const CsoArgs& a, cudaStream_t st);

@@ -9,7 +9,7 @@
 //
 // Row engine geometry (a function of ld only, so every result is bitwise the
 // same for every shard count, R-11):
-//   * LPR lanes walk one row (LPR = 8 for ld <= 256, else 32); a warp holds
+//   * LPR lanes walk one row (LPR = 4 / 8 for ld <= 128 / 256, else 32); a warp holds
 //     RPW = 32/LPR consecutive rows; or
 //   * WPR = 8 warps (one CTA) share one row, each owning a contiguous segment
 //     (ld > 4096).
@@ -57,6 +57,13 @@ __device__ __forceinline__ void row_segment(long long NQ, int wpr, int wr, long 
 __device__ __forceinline__ float4 bound4(const float* b, float b0, int uniform, long long q) {
     if (uniform) return make_float4(b0, b0, b0, b0);
     return __ldg(reinterpret_cast<const float4*>(b) + q);
+}
+// Compile-time specialisation: uniform bounds feed FMNMX straight from the
+// constant bank; per-column bounds are two L1-resident LDG.128 per quad.
+template <bool UNI>
+__device__ __forceinline__ float4 bound4t(const float* b, float b0, long long q) {
+    if constexpr (UNI) return make_float4(b0, b0, b0, b0);
+    else return __ldg(reinterpret_cast<const float4*>(b) + q);
 }
 
 __device__ __forceinline__ float clipf(float x, float lo, float hi) {
@@ -260,6 +267,7 @@ struct MoverEval {
 // PSO move of one row (A1, A3, A4, lazy A5).  Holds a reference to the kernel
 // parameter block (resolved to constant-bank operands once inlined: the
 // Philox round keys, w, phi*2^-24 and the bounds feed instructions directly).
+template <bool UNI, bool G_COHERENT = false>
 struct MoverPso {
     const PsoArgs& a;
     float4* Xr;
@@ -287,9 +295,12 @@ struct MoverPso {
         const float4 xo = x[u];
         const float4 pb = pend ? xo : p[u];
         if (pend) st_stream(Pr + q, xo);
-        const float4 g = __ldg(reinterpret_cast<const float4*>(a.G) + q);
-        const float4 lo = bound4(a.lb, a.lb0, a.uniform_bounds, q);
-        const float4 hi = bound4(a.ub, a.ub0, a.uniform_bounds, q);
+        // G is read-only for a generation kernel (non-coherent path); the
+        // persistent small-population kernel rewrites it between generations.
+        const float4 g = G_COHERENT ? __ldcg(reinterpret_cast<const float4*>(a.G) + q)
+                                    : __ldg(reinterpret_cast<const float4*>(a.G) + q);
+        const float4 lo = bound4t<UNI>(a.lb, a.lb0, q);
+        const float4 hi = bound4t<UNI>(a.ub, a.ub0, q);
         const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 2u), a.rk);
         const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 3u), a.rk);
         float4 xn = xo, vn = v[u];
@@ -486,7 +497,7 @@ __global__ void __launch_bounds__(256) k_eval(const float* __restrict__ X, long 
 }
 
 // Fused PSO generation: lazy pbest + move + clip + evaluate + tell + argmin.
-template <int P, class G>
+template <int P, class G, bool UNI>
 __global__ void __launch_bounds__(256, 2) k_pso_gen(PsoArgs a) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
@@ -505,7 +516,7 @@ __global__ void __launch_bounds__(256, 2) k_pso_gen(PsoArgs a) {
     wp.ld_bytes = a.ld * 4;
     wp.qb = m.qb;
     wp.seg = seg;
-    wp.ahead = seg < 2 * G::GROUP ? seg : 2 * G::GROUP;
+    wp.ahead = seg < 4 * G::GROUP ? seg : 4 * G::GROUP;
     wp.on = !mode_a && lane == 0;
     wp.c = 0;
     unsigned long long best = ~0ull;
@@ -543,7 +554,7 @@ __global__ void __launch_bounds__(256, 2) k_pso_gen(PsoArgs a) {
         const bool pend_nn = nn < a.rows ? a.imp[nn] != 0 : true;
         float pf_old = 0.0f;
         if (m.leader && ok) pf_old = a.pf[row];
-        MoverPso mv(a, ok ? row : 0, (uint32_t)t, pend_cur);
+        MoverPso<UNI> mv(a, ok ? row : 0, (uint32_t)t, pend_cur);
         Fit<P> acc;
         float hx, tx;
         bool tv;
@@ -566,8 +577,87 @@ __global__ void __launch_bounds__(256, 2) k_pso_gen(PsoArgs a) {
     if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
 }
 
+
+// Persistent single-CTA PSO for tiny populations (latency-bound, e.g. C1:
+// 100 x 10): all n generations in one launch, a CTA barrier instead of the
+// grid-wide argmin.  Per-row arithmetic, reduction order and decisions are
+// those of k_pso_gen, so the trajectory is bitwise identical.
+template <int P, class G, bool UNI>
+__global__ void __launch_bounds__(256) k_pso_run_small(PsoArgs a, long long n_gens) {
+    __shared__ Fit<P> sh_acc[G::WPR];
+    __shared__ float sh_head[G::WPR];
+    __shared__ __align__(16) HStore<P> sh_h;
+    __shared__ unsigned long long sh_k[WARPS];
+    __shared__ int sh_better;
+    __shared__ long long sh_row;
+    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+    const RowMap<G> m(a.ld >> 2);
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    Ctl* ctl = a.ctl;
+    unsigned long long t = ctl->t;
+    float gf = ctl->gf;
+    long long gidx = ctl->gidx;
+    NoPrefetch pf;
+    for (long long g = 0; g < n_gens; ++g) {
+        unsigned long long best = ~0ull;
+        for (long long it = 0;; ++it) {
+            const long long wrow = m.wfirst + it * m.stride;
+            if (wrow >= a.rows) break;
+            const long long row = m.first + it * m.stride;
+            const bool ok = row < a.rows;
+            const bool pend = ok ? a.imp[row] != 0 : true;
+            float pf_old = 0.0f;
+            if (m.leader && ok) pf_old = a.pf[row];
+            MoverPso<UNI, true> mv(a, ok ? row : 0, (uint32_t)t, pend);
+            Fit<P> acc;
+            float hx, tx;
+            bool tv;
+            walk_segment<P, G>(mv, m.qb, m.qe, a.D, ok, acc, hx, tx, tv, pf, htab);
+            const float f = reduce_row<P, G>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
+            if (m.leader && ok) {
+                const bool imp = f < pf_old;
+                a.f[row] = f;
+                a.imp[row] = imp ? 1 : 0;
+                if (imp) a.pf[row] = f;
+                const unsigned long long k = make_key(f, a.row0 + row);
+                best = k < best ? k : best;
+            }
+        }
+        best = warp_min_u64(best);
+        if (lane == 0) sh_k[wid] = best;
+        __syncthreads();  // also orders this generation's X stores before the G copy
+        if (threadIdx.x == 0) {
+            unsigned long long k = sh_k[0];
+            for (int i = 1; i < WARPS; ++i) k = sh_k[i] < k ? sh_k[i] : k;
+            const bool any = k != ~0ull;
+            const float fmin = any ? unord_f32((uint32_t)(k >> 32)) : __int_as_float(0x7f800000);
+            const bool better = any && fmin < gf;  // strict improvement
+            sh_better = better;
+            sh_row = (long long)(uint32_t)(k & 0xffffffffu) - a.row0;
+            if (better) {
+                gf = fmin;
+                gidx = (long long)(uint32_t)(k & 0xffffffffu);
+            }
+            ctl->hist[t + 1] = fmin;
+        }
+        __syncthreads();
+        if (sh_better) {
+            const float4* src = reinterpret_cast<const float4*>(a.X + sh_row * a.ld);
+            float4* Gd = reinterpret_cast<float4*>(a.G);
+            for (long long q = threadIdx.x; q < (a.ld >> 2); q += blockDim.x) Gd[q] = __ldcg(src + q);
+        }
+        __syncthreads();
+        ++t;
+    }
+    if (threadIdx.x == 0) {
+        ctl->t = t;
+        ctl->gf = gf;
+        ctl->gidx = gidx;
+    }
+}
+
 // Unfused ask: move X_t -> X_{t+1} (no evaluation).
-template <class G>
+template <class G, bool UNI>
 __global__ void __launch_bounds__(256) k_pso_move(PsoArgs a, unsigned long long t) {
     __shared__ Fit<SPHERE> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
@@ -581,7 +671,7 @@ __global__ void __launch_bounds__(256) k_pso_move(PsoArgs a, unsigned long long 
         const long long row = m.first + it * m.stride;
         const bool ok = row < a.rows;
         const bool pend = ok ? a.imp[row] != 0 : false;
-        MoverPso mv(a, ok ? row : 0, (uint32_t)t, pend);
+        MoverPso<UNI> mv(a, ok ? row : 0, (uint32_t)t, pend);
         Fit<SPHERE> acc;  // unused
         float hx, tx;
         bool tv;
@@ -701,6 +791,7 @@ struct CsoPerm {
 };
 
 // Loser update of one row (A15): v = fmaf(R2, xw-xl, R1*vl) [+ phi R3 (xbar-xl)], clip.
+template <bool UNI>
 struct MoverCso {
     const CsoArgs& a;
     float4* Xl;
@@ -734,8 +825,8 @@ struct MoverCso {
                              __fmul_rn(phi, u24(b3.z)), __fmul_rn(phi, u24(b3.w)));
             xb = __ldg(reinterpret_cast<const float4*>(a.xbar) + q);
         }
-        const float4 lo = bound4(a.lb, a.lb0, a.uniform_bounds, q);
-        const float4 hi = bound4(a.ub, a.ub0, a.uniform_bounds, q);
+        const float4 lo = bound4t<UNI>(a.lb, a.lb0, q);
+        const float4 hi = bound4t<UNI>(a.ub, a.ub0, q);
         float4 xn, vn;
         xn.x = upd(x[u].x, v[u].x, xw[u].x, u24(b1.x), u24(b2.x), c3.x, xb.x, use3, lo.x, hi.x, vn.x);
         xn.y = upd(x[u].y, v[u].y, xw[u].y, u24(b1.y), u24(b2.y), c3.y, xb.y, use3, lo.y, hi.y, vn.y);
@@ -806,7 +897,7 @@ __device__ __forceinline__ CsoItem cso_item(const CsoArgs& a, long long it, uint
 
 // One CSO generation over this shard's whole blocks.  One work item per pair
 // (plus one for the unpaired member of an odd block), mapped like a row.
-template <int P, class G>
+template <int P, class G, bool UNI>
 __global__ void __launch_bounds__(256, 2) k_cso_gen(CsoArgs a) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
@@ -819,15 +910,34 @@ __global__ void __launch_bounds__(256, 2) k_cso_gen(CsoArgs a) {
     const long long items = nblk * ((a.B + 1) / 2);
     NoPrefetch pf;
     unsigned long long best = ~0ull;
+    const long long seg_off = m.qb * 16, seg_bytes = (m.qe - m.qb) * 16;
+    // Items are resolved two iterations ahead: the pair's fitness loads land
+    // during one iteration, the winner/loser rows are prefetched into L2 during
+    // the next (the rows are scattered by the pairing, so there is no stream
+    // to follow).  Pairs are disjoint, so no other item of this generation
+    // writes the fitness read here.
+    CsoItem ci_cur, ci_nxt;
+    ci_cur.valid = false;
+    ci_nxt.valid = false;
+    if (m.first < items) ci_cur = cso_item(a, m.first, (uint32_t)t);
+    if (m.first + m.stride < items) ci_nxt = cso_item(a, m.first + m.stride, (uint32_t)t);
     for (long long k = 0;; ++k) {
         const long long witem = m.wfirst + k * m.stride;
         if (witem >= items) break;
         const long long it = m.first + k * m.stride;
-        CsoItem ci;
-        ci.valid = false;
-        if (it < items) ci = cso_item(a, it, (uint32_t)t);
+        if (m.sl == 0 && ci_nxt.valid && ci_nxt.gl >= 0) {
+            const char* X = reinterpret_cast<const char*>(a.X);
+            const long long ol = (ci_nxt.gl - a.row0) * a.ld * 4 + seg_off;
+            prefetch_l2(X + ol, seg_bytes);
+            prefetch_l2(reinterpret_cast<const char*>(a.V) + ol, seg_bytes);
+            prefetch_l2(X + (ci_nxt.gw - a.row0) * a.ld * 4 + seg_off, seg_bytes);
+        }
+        CsoItem ci_nn;
+        ci_nn.valid = false;
+        if (it + 2 * m.stride < items) ci_nn = cso_item(a, it + 2 * m.stride, (uint32_t)t);
+        const CsoItem ci = ci_cur;
         const bool pair = ci.valid && ci.gl >= 0;
-        MoverCso mv(a);
+        MoverCso<UNI> mv(a);
         const long long lrow = pair ? ci.gl - a.row0 : 0, wrow = pair ? ci.gw - a.row0 : 0;
         mv.Xl = reinterpret_cast<float4*>(a.X + lrow * a.ld);
         mv.Vl = reinterpret_cast<float4*>(a.V + lrow * a.ld);
@@ -848,6 +958,8 @@ __global__ void __launch_bounds__(256, 2) k_cso_gen(CsoArgs a) {
             }
             best = kk < best ? kk : best;
         }
+        ci_cur = ci_nxt;
+        ci_nxt = ci_nn;
     }
     unsigned long long key;
     if (grid_argmin(a.ctl, best, &key)) cso_finalize(a, key, t + 1);
@@ -933,13 +1045,17 @@ int sm_count(int device) {
     return n;
 }
 
+using G4 = Geom<4, 1>;
 using G8 = Geom<8, 1>;
 using G32 = Geom<32, 1>;
 using GW8 = Geom<32, 8>;
 
-// 0: 8 lanes per row (ld <= 256), 1: a warp per row (ld <= 4096), 2: a CTA per row.
+// 3: 4 lanes per row (ld <= 128), 0: 8 lanes per row (ld <= 256), 1: a warp per
+// row (ld <= 4096), 2: a CTA per row.  Narrow row groups keep short rows from
+// idling lanes (dim 100 = 25 quads: 28 lane-slots with 4 lanes vs 32 with 8).
 int geom_id(long long ld) {
     const long long NQ = ld >> 2;
+    if (NQ <= 32) return 3;
     if (NQ <= 64) return 0;
     if (NQ <= 1024) return 1;
     return 2;
@@ -961,6 +1077,10 @@ int wpr_for_dim(long long ld) { return geom_id(ld) == 2 ? 8 : 1; }
 #define EVOX_DISPATCH_GEOM(ld, ...)     \
     do {                                \
         switch (geom_id(ld)) {          \
+            case 3: {                   \
+                using G_ = G4;          \
+                __VA_ARGS__;            \
+            } break;                    \
             case 0: {                   \
                 using G_ = G8;          \
                 __VA_ARGS__;            \
@@ -1002,6 +1122,17 @@ int wpr_for_dim(long long ld) { return geom_id(ld) == 2 ? 8 : 1; }
         }                                      \
     } while (0)
 
+#define EVOX_DISPATCH_UNI(u, ...)         \
+    do {                                  \
+        if (u) {                          \
+            constexpr bool U_ = true;     \
+            __VA_ARGS__;                  \
+        } else {                          \
+            constexpr bool U_ = false;    \
+            __VA_ARGS__;                  \
+        }                                 \
+    } while (0)
+
 template <class G>
 static long long row_units(long long rows) {
     return (rows + G::RPC - 1) / G::RPC;
@@ -1031,25 +1162,34 @@ cudaError_t launch_eval(int problem, const float* X, long long rows, long long D
 int pso_gen_grid(int problem, long long ld, long long rows, int device) {
     int g = 1;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
-        g = grid_for((const void*)k_pso_gen<P_, G_>, row_units<G_>(rows), device);
+        g = grid_for((const void*)k_pso_gen<P_, G_, true>, row_units<G_>(rows), device);
     }));
     return g;
 }
 
 cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st) {
-    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-        k_pso_gen<P_, G_><<<grid, 256, 0, st>>>(a);
-    }));
+    EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+        k_pso_gen<P_, G_, U_><<<grid, 256, 0, st>>>(a);
+    })));
+    return cudaGetLastError();
+}
+
+bool pso_small(long long rows, long long ld) { return rows * ld <= 65536; }
+
+cudaError_t launch_pso_run_small(int problem, const PsoArgs& a, long long n, cudaStream_t st) {
+    EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+        k_pso_run_small<P_, G_, U_><<<1, 256, 0, st>>>(a, n);
+    })));
     return cudaGetLastError();
 }
 
 cudaError_t launch_pso_move(const PsoArgs& a, unsigned long long t, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
-    EVOX_DISPATCH_GEOM(a.ld, {
-        const int g = grid_for((const void*)k_pso_move<G_>, row_units<G_>(a.rows), dev);
-        k_pso_move<G_><<<g, 256, 0, st>>>(a, t);
-    });
+    EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_GEOM(a.ld, {
+        const int g = grid_for((const void*)k_pso_move<G_, U_>, row_units<G_>(a.rows), dev);
+        k_pso_move<G_, U_><<<g, 256, 0, st>>>(a, t);
+    }));
     return cudaGetLastError();
 }
 
@@ -1101,15 +1241,15 @@ static long long cso_items(const CsoArgs& a) {
 int cso_gen_grid(int problem, const CsoArgs& a, int device) {
     int g = 1;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-        g = grid_for((const void*)k_cso_gen<P_, G_>, row_units<G_>(cso_items(a)), device);
+        g = grid_for((const void*)k_cso_gen<P_, G_, true>, row_units<G_>(cso_items(a)), device);
     }));
     return g;
 }
 
 cudaError_t launch_cso_gen(int problem, const CsoArgs& a, int grid, cudaStream_t st) {
-    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-        k_cso_gen<P_, G_><<<grid, 256, 0, st>>>(a);
-    }));
+    EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+        k_cso_gen<P_, G_, U_><<<grid, 256, 0, st>>>(a);
+    })));
     return cudaGetLastError();
 }
 

@@ -167,6 +167,21 @@ def test_pso_graphed_equals_stepwise(problem, N, D, lb, ub, seed):
     assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
 
 
+@pytest.mark.parametrize("problem,N,D,lb,ub,seed", PSO_CASES[:5])
+def test_pso_small_kernel_equals_grid_kernel(problem, N, D, lb, ub, seed, monkeypatch):
+    """The persistent single-CTA kernel (tiny populations) is bitwise identical to the
+    multi-CTA generation kernel."""
+    a = ev.PSO(N, D, lb, ub, seed=seed)
+    a.step(problem, 60)
+    monkeypatch.setenv("EVOX_NO_SMALL", "1")
+    b = ev.PSO(N, D, lb, ub, seed=seed)
+    b.step(problem, 60)
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
+        assert np.array_equal(ga[k], gb[k]), k
+    assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
+
+
 def test_pso_c1_oneshot_matches_oracle():
     """C1 (PSO/Sphere 100x10, 100 generations, seed 0) in one step(100) call."""
     pso = ev.PSO(100, 10, -5.12, 5.12, seed=0)
