@@ -29,7 +29,13 @@ namespace evox {
 
 namespace {
 
-constexpr int U = 4;               // chunks in flight per lane group
+#ifndef EVOX_U
+#define EVOX_U 4
+#endif
+#ifndef EVOX_MINB
+#define EVOX_MINB 2
+#endif
+constexpr int U = EVOX_U;          // chunks in flight per lane group
 constexpr int WARPS = 8;           // warps per CTA (256 threads) in every geometry
 constexpr long long MODE_A_MAX = 384;  // quads per warp-iteration prefetched whole (mode A)
 constexpr unsigned FULL = 0xffffffffu;
@@ -108,11 +114,15 @@ struct HTable {
 template <class G>
 struct HTable<GRIEWANK, G> {
     __device__ __forceinline__ static const float* fill(float* sh, long long ld) {
-        if (G::WPR > 1 || ld > HTAB) return nullptr;
-        for (long long j = threadIdx.x; j < ld; j += blockDim.x)
-            sh[j] = (float)(0.15915494309189534 / sqrt((double)(j + 1)));
-        __syncthreads();
-        return sh;
+        if constexpr (G::WPR > 1) {
+            return nullptr;
+        } else {
+            if (ld > HTAB) return nullptr;
+            for (long long j = threadIdx.x; j < ld; j += blockDim.x)
+                sh[j] = (float)(0.15915494309189534 / sqrt((double)(j + 1)));
+            __syncthreads();
+            return sh;
+        }
     }
 };
 template <int P>
@@ -498,7 +508,7 @@ __global__ void __launch_bounds__(256) k_eval(const float* __restrict__ X, long 
 
 // Fused PSO generation: lazy pbest + move + clip + evaluate + tell + argmin.
 template <int P, class G, bool UNI>
-__global__ void __launch_bounds__(256, 2) k_pso_gen(PsoArgs a) {
+__global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen(PsoArgs a) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
     __shared__ __align__(16) HStore<P> sh_h;
@@ -898,7 +908,7 @@ __device__ __forceinline__ CsoItem cso_item(const CsoArgs& a, long long it, uint
 // One CSO generation over this shard's whole blocks.  One work item per pair
 // (plus one for the unpaired member of an odd block), mapped like a row.
 template <int P, class G, bool UNI>
-__global__ void __launch_bounds__(256, 2) k_cso_gen(CsoArgs a) {
+__global__ void __launch_bounds__(256, EVOX_MINB) k_cso_gen(CsoArgs a) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
     __shared__ __align__(16) HStore<P> sh_h;

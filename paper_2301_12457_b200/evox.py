@@ -18,7 +18,8 @@ from typing import Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libevox.so")
+# EVOX_LIB selects a tuning variant built by _build.build(defines=...) (in-tree)
+LIB_PATH = os.environ.get("EVOX_LIB") or os.path.join(_PKG, "libevox.so")
 
 PROBLEMS = {"sphere": 0, "ackley": 1, "rastrigin": 2, "griewank": 3, "rosenbrock": 4}
 DEFAULT_BOUNDS = {"sphere": (-5.12, 5.12), "ackley": (-32.768, 32.768),
