@@ -187,10 +187,12 @@ evox_status evox_pso_sync(evox_pso* s);
  * instead of through CUDA graphs.  kernel_time synchronises and returns the
  * summed device time in ms and the number of generations those launches ran
  * since the last reset (one per launch, except the persistent small-population
- * kernel, which runs all n generations of a step in one launch); reset != 0
- * clears the counters after reading. */
+ * kernel, which runs all n generations of a step in one launch) and the
+ * number of those launches (NULL pointers are skipped); reset != 0 clears
+ * the counters after reading. */
 evox_status evox_pso_set_timing(evox_pso* s, int enable);
-evox_status evox_pso_kernel_time(evox_pso* s, double* total_ms, int64_t* gens, int reset);
+evox_status evox_pso_kernel_time(evox_pso* s, double* total_ms, int64_t* gens, int64_t* launches,
+                                 int reset);
 
 /* Release the handle (never fails for a valid or poisoned handle; NULL ok). */
 evox_status evox_pso_destroy(evox_pso* s);
@@ -219,7 +221,8 @@ evox_status evox_cso_load(evox_cso* s, const void* host_blob, size_t size);
 evox_status evox_cso_save(evox_cso* s, void* host_blob, size_t cap, size_t* used);
 evox_status evox_cso_sync(evox_cso* s);
 evox_status evox_cso_set_timing(evox_cso* s, int enable);
-evox_status evox_cso_kernel_time(evox_cso* s, double* total_ms, int64_t* gens, int reset);
+evox_status evox_cso_kernel_time(evox_cso* s, double* total_ms, int64_t* gens, int64_t* launches,
+                                 int reset);
 evox_status evox_cso_destroy(evox_cso* s);
 
 /* ---------------------------------------------------------------- test hooks */

@@ -78,7 +78,8 @@ struct Base {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
     std::vector<int64_t> ev_gens;
     double kernel_ms = 0.0;
-    int64_t kernel_n = 0;
+    int64_t kernel_n = 0;        // generations run by the timed launches
+    int64_t kernel_launches = 0;
 };
 
 // Timed launch: events around the kernel enqueued by `launch`, which runs
@@ -112,6 +113,7 @@ cudaError_t collect_timing(Base* b) {
         if (e != cudaSuccess) return e;
         b->kernel_ms += ms;
         b->kernel_n += b->ev_gens[i];
+        b->kernel_launches += 1;
         b->ev_free.push_back(ev);
     }
     b->ev_pending.clear();
@@ -850,7 +852,8 @@ evox_status evox_pso_set_timing(evox_pso* s, int enable) {
     return EVOX_OK;
 }
 
-evox_status evox_pso_kernel_time(evox_pso* s, double* total_ms, int64_t* launches, int reset) {
+evox_status evox_pso_kernel_time(evox_pso* s, double* total_ms, int64_t* gens, int64_t* launches,
+                                 int reset) {
     evox_status st = check_pso(s);
     if (st != EVOX_OK) return st;
     st = sync_check(s);
@@ -858,10 +861,12 @@ evox_status evox_pso_kernel_time(evox_pso* s, double* total_ms, int64_t* launche
     DevGuard g(s->device);
     CU(s, collect_timing(s));
     if (total_ms) *total_ms = s->kernel_ms;
-    if (launches) *launches = s->kernel_n;
+    if (gens) *gens = s->kernel_n;
+    if (launches) *launches = s->kernel_launches;
     if (reset) {
         s->kernel_ms = 0.0;
         s->kernel_n = 0;
+        s->kernel_launches = 0;
     }
     return EVOX_OK;
 }
@@ -1209,7 +1214,8 @@ evox_status evox_cso_set_timing(evox_cso* s, int enable) {
     return EVOX_OK;
 }
 
-evox_status evox_cso_kernel_time(evox_cso* s, double* total_ms, int64_t* launches, int reset) {
+evox_status evox_cso_kernel_time(evox_cso* s, double* total_ms, int64_t* gens, int64_t* launches,
+                                 int reset) {
     evox_status st = check_cso(s);
     if (st != EVOX_OK) return st;
     st = sync_check(s);
@@ -1217,10 +1223,12 @@ evox_status evox_cso_kernel_time(evox_cso* s, double* total_ms, int64_t* launche
     DevGuard g(s->device);
     CU(s, collect_timing(s));
     if (total_ms) *total_ms = s->kernel_ms;
-    if (launches) *launches = s->kernel_n;
+    if (gens) *gens = s->kernel_n;
+    if (launches) *launches = s->kernel_launches;
     if (reset) {
         s->kernel_ms = 0.0;
         s->kernel_n = 0;
+        s->kernel_launches = 0;
     }
     return EVOX_OK;
 }

@@ -85,7 +85,7 @@ SIGNATURES = {
     "evox_pso_sync": ([_p], _i),
     "evox_pso_destroy": ([_p], _i),
     "evox_pso_set_timing": ([_p, _i], _i),
-    "evox_pso_kernel_time": ([_p, ctypes.POINTER(ctypes.c_double), _PI64, _i], _i),
+    "evox_pso_kernel_time": ([_p, ctypes.POINTER(ctypes.c_double), _PI64, _PI64, _i], _i),
     "evox_cso_workspace_bytes": ([_i64, _i64, _i, _i, _PSZ], _i),
     "evox_cso_init": ([_i64, _i64, _p, _p, _f32, _i64, _u64, _p, _PP], _i),
     "evox_cso_step": ([_p, _i, _i64], _i),
@@ -98,7 +98,7 @@ SIGNATURES = {
     "evox_cso_sync": ([_p], _i),
     "evox_cso_destroy": ([_p], _i),
     "evox_cso_set_timing": ([_p, _i], _i),
-    "evox_cso_kernel_time": ([_p, ctypes.POINTER(ctypes.c_double), _PI64, _i], _i),
+    "evox_cso_kernel_time": ([_p, ctypes.POINTER(ctypes.c_double), _PI64, _PI64, _i], _i),
     "evox_debug_philox": ([_p, _u32, _u32, _p, _i64, _p], _i),
 }
 
@@ -287,11 +287,12 @@ class _Handle:
         """Bracket every generation kernel with CUDA events (launches un-graphed)."""
         _check(self._fn("set_timing")(self._h, int(bool(enable))))
 
-    def kernel_time(self, reset: bool = False) -> tuple[float, int]:
-        """(summed generation-kernel device time in ms, number of timed launches)."""
-        ms, n = ctypes.c_double(), ctypes.c_int64()
-        _check(self._fn("kernel_time")(self._h, ctypes.byref(ms), ctypes.byref(n), int(reset)))
-        return ms.value, n.value
+    def kernel_time(self, reset: bool = False) -> tuple[float, int, int]:
+        """(summed generation-kernel device time in ms, generations they ran, launches)."""
+        ms, n, k = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
+        _check(self._fn("kernel_time")(self._h, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(k),
+                                       int(reset)))
+        return ms.value, n.value, k.value
 
     def history(self) -> np.ndarray:
         n = ctypes.c_int64()
