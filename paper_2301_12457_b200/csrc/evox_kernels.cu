@@ -21,8 +21,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdlib>
-#include <type_traits>
 
 #include "evox_device.cuh"
 #include "evox_internal.h"
@@ -589,211 +587,6 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen(PsoArgs a) {
     if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
 }
 
-
-// Streaming variant of the fused PSO generation.  Each lane keeps a ring of U
-// register slots; after computing the chunk in slot u it immediately refills
-// the slot with the chunk U positions further along the warp's stream of rows
-// (crossing into its next row), so U-1..U chunks of loads are always in
-// flight instead of draining at the end of every lane group.  Same per-element
-// arithmetic, per-row reduction tree and decisions as k_pso_gen (bitwise
-// identical; tested).  Used when a row segment has at least U chunks.
-template <bool UNI>
-struct PsoSlots {
-    const PsoArgs& a;
-    float4 x[U], v[U], p[U];
-    __device__ __forceinline__ explicit PsoSlots(const PsoArgs& a_) : a(a_) {}
-    template <int u>
-    __device__ __forceinline__ void load(long long row, long long q, bool pend) {
-        const long long o = row * (a.ld >> 2) + q;
-        x[u] = ld_stream(reinterpret_cast<const float4*>(a.X) + o);
-        v[u] = ld_stream(reinterpret_cast<const float4*>(a.V) + o);
-        if (!pend) p[u] = ld_stream(reinterpret_cast<const float4*>(a.P) + o);
-    }
-    template <int u>
-    __device__ __forceinline__ float4 step(long long row, long long q, bool pend, uint32_t row_g,
-                                           uint32_t t) {
-        const long long o = row * (a.ld >> 2) + q;
-        const float4 xo = x[u];
-        const float4 pb = pend ? xo : p[u];
-        if (pend) st_stream(reinterpret_cast<float4*>(a.P) + o, xo);
-        const float4 g = __ldg(reinterpret_cast<const float4*>(a.G) + q);
-        const float4 lo = bound4t<UNI>(a.lb, a.lb0, q);
-        const float4 hi = bound4t<UNI>(a.ub, a.ub0, q);
-        const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 2u), a.rk);
-        const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 3u), a.rk);
-        float4 xn = xo, vn = v[u];
-        const float w = a.w, cp = a.cp, cg = a.cg;
-        pso_elem(xn.x, vn.x, pb.x, g.x, scaled_u24(b1.x, cp), scaled_u24(b2.x, cg), w, lo.x, hi.x);
-        pso_elem(xn.y, vn.y, pb.y, g.y, scaled_u24(b1.y, cp), scaled_u24(b2.y, cg), w, lo.y, hi.y);
-        pso_elem(xn.z, vn.z, pb.z, g.z, scaled_u24(b1.z, cp), scaled_u24(b2.z, cg), w, lo.z, hi.z);
-        pso_elem(xn.w, vn.w, pb.w, g.w, scaled_u24(b1.w, cp), scaled_u24(b2.w, cg), w, lo.w, hi.w);
-        zero_pad(xn, vn, q, a.D);
-        st_stream(reinterpret_cast<float4*>(a.X) + o, xn);
-        st_stream(reinterpret_cast<float4*>(a.V) + o, vn);
-        return xn;
-    }
-};
-
-template <int P, class G, bool UNI>
-__global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen_stream(PsoArgs a) {
-    __shared__ Fit<P> sh_acc[G::WPR];
-    __shared__ float sh_head[G::WPR];
-    __shared__ __align__(16) HStore<P> sh_h;
-    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
-    const RowMap<G> m(a.ld >> 2);
-    const int lane = lane_id();
-    const int sl = m.sl;
-    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
-    const long long NQ = a.ld >> 2;
-    const long long seg = m.qe - m.qb;
-    // chunks per row segment: the NOMINAL segment, identical for every warp of
-    // a row (row ends must be CTA-uniform when WPR > 1); lanes mask q >= qe.
-    const long long nseg = (NQ + G::WPR - 1) / G::WPR;
-    const long long NC = (nseg + G::LPR - 1) / G::LPR;
-    const long long n_it = m.wfirst < a.rows ? (a.rows - 1 - m.wfirst) / m.stride + 1 : 0;
-    const long long total = n_it * NC;  // chunks in this warp's stream
-    const bool mode_a = seg * G::RPW <= MODE_A_MAX;
-    WindowPrefetch wp;
-    wp.X = reinterpret_cast<const char*>(a.X);
-    wp.V = reinterpret_cast<const char*>(a.V);
-    wp.P = reinterpret_cast<const char*>(a.P);
-    wp.ld_bytes = a.ld * 4;
-    wp.qb = m.qb;
-    wp.seg = seg;
-    wp.ahead = seg < 4 * G::GROUP ? seg : 4 * G::GROUP;
-    wp.on = !mode_a && lane == 0;
-    wp.c = 0;
-
-    // compute cursor (row iteration ci, chunk cc) and load cursor (li, lc)
-    long long ci = 0, cc = 0, li = 0, lc = 0;
-    long long crow = m.first;
-    // pbest-pending flags of the compute row and the next two rows of the
-    // stream (the load cursor is never more than one row ahead: NC >= U)
-    bool p_c = crow < a.rows ? a.imp[crow] != 0 : true;
-    bool p_n = crow + m.stride < a.rows ? a.imp[crow + m.stride] != 0 : true;
-    bool p_nn = crow + 2 * m.stride < a.rows ? a.imp[crow + 2 * m.stride] != 0 : true;
-    float pf_old = 0.0f;
-    if (m.leader && crow < a.rows) pf_old = a.pf[crow];
-    PsoSlots<UNI> sl_(a);
-    Fit<P> acc;
-    float pend_x = 0.0f, head_x = 0.0f, tail_x = 0.0f;
-    bool hpend = false, tail_valid = false;
-    unsigned long long best = ~0ull;
-
-    auto issue = [&](auto uc) {  // load the chunk at the load cursor into slot uc
-        constexpr int u = decltype(uc)::value;
-        const long long lrow = m.first + li * m.stride;
-        const long long q = m.qb + lc * G::LPR + sl;
-        if (lrow < a.rows && q < m.qe) sl_.template load<u>(lrow, q, li == ci ? p_c : p_n);
-        if (++lc == NC) { lc = 0; ++li; }
-    };
-    auto row_start = [&]() {  // prefetch for the row the compute cursor enters
-        const long long nxt = crow + m.stride;
-        if (mode_a) {
-            const long long wn = m.wfirst + (ci + 1) * m.stride;
-            if (lane == 0 && wn < a.rows) {
-                const long long nr = a.rows - wn < G::RPW ? a.rows - wn : G::RPW;
-                const long long o = wn * a.ld * 4 + m.qb * 16;
-                const long long bytes = G::WPR == 1 ? nr * a.ld * 4 : seg * 16;
-                prefetch_l2(reinterpret_cast<const char*>(a.X) + o, bytes);
-                prefetch_l2(reinterpret_cast<const char*>(a.V) + o, bytes);
-            }
-            if (sl == 0 && nxt < a.rows && !p_n)
-                prefetch_l2(reinterpret_cast<const char*>(a.P) + nxt * a.ld * 4 + m.qb * 16,
-                            seg * 16);
-        } else {
-            wp.row = crow;
-            wp.nxt = nxt < a.rows ? nxt : -1;
-            wp.pend_cur = p_c;
-            wp.pend_nxt = p_n;
-        }
-    };
-
-    if (total > 0) row_start();
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-        if (u < total) {
-            if (u == 0) issue(std::integral_constant<int, 0>{});
-            if (u == 1) issue(std::integral_constant<int, 1>{});
-            if (u == 2) issue(std::integral_constant<int, 2>{});
-            if (u == 3) issue(std::integral_constant<int, 3>{});
-        }
-
-    auto chunk = [&](auto uc, long long s) {
-        constexpr int u = decltype(uc)::value;
-        const bool c_ok = crow < a.rows;
-        const long long cb = m.qb + cc * G::LPR;
-        if (cc % U == 0) wp(cb);
-        const long long q = cb + sl;
-        const bool valid = c_ok && q < m.qe;
-        float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) {
-            xn = sl_.template step<u>(crow, q, p_c, (uint32_t)(a.row0 + crow), (uint32_t)t);
-            fit_quad<P>(acc, xn, 4 * q, a.D, htab);
-        }
-        if constexpr (P == ROSENBROCK) {
-            const float nb = __shfl_down_sync(FULL, xn.x, 1, G::LPR);
-            const float f0 = __shfl_sync(FULL, xn.x, 0, G::LPR);
-            if (cc == 0) head_x = f0;
-            if (sl == G::LPR - 1 && hpend) {
-                acc.pair(pend_x, f0);
-                hpend = false;
-            }
-            if (valid) {
-                const bool has_next = 4 * q + 4 < a.D;
-                if (q + 1 < m.qe) {
-                    if (sl < G::LPR - 1) {
-                        if (has_next) acc.pair(xn.w, nb);
-                    } else {
-                        hpend = has_next;
-                        pend_x = xn.w;
-                    }
-                } else {
-                    tail_valid = has_next;
-                    tail_x = xn.w;
-                }
-            }
-        }
-        // refill this slot with the chunk U positions ahead (possibly the next row)
-        if (s + U < total) issue(uc);
-        if (cc == NC - 1) {  // end of the row (warp-uniform; CTA-uniform for WPR > 1)
-            const float f = reduce_row<P, G>(acc, a.D, head_x, tail_x, tail_valid, sh_acc, sh_head);
-            if (m.leader && c_ok) {
-                const bool imp = f < pf_old;  // per-row tell (A11)
-                a.f[crow] = f;
-                a.imp[crow] = imp ? 1 : 0;
-                if (imp) a.pf[crow] = f;
-                const unsigned long long k = make_key(f, a.row0 + crow);
-                best = k < best ? k : best;
-            }
-            acc = Fit<P>();
-            hpend = false;
-            tail_valid = false;
-            head_x = tail_x = pend_x = 0.0f;
-            ++ci;
-            cc = 0;
-            crow += m.stride;
-            p_c = p_n;
-            p_n = p_nn;
-            const long long r3 = crow + 2 * m.stride;
-            p_nn = r3 < a.rows ? a.imp[r3] != 0 : true;
-            if (m.leader && crow < a.rows) pf_old = a.pf[crow];
-            wp.c = wp.c > seg ? wp.c - seg : 0;
-            if (ci < n_it) row_start();
-        } else {
-            ++cc;
-        }
-    };
-
-    for (long long s0 = 0; s0 < total; s0 += U) {
-        chunk(std::integral_constant<int, 0>{}, s0);
-        if (s0 + 1 < total) chunk(std::integral_constant<int, 1>{}, s0 + 1);
-        if (s0 + 2 < total) chunk(std::integral_constant<int, 2>{}, s0 + 2);
-        if (s0 + 3 < total) chunk(std::integral_constant<int, 3>{}, s0 + 3);
-    }
-    unsigned long long key;
-    if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
-}
 
 // Persistent single-CTA PSO for tiny populations (latency-bound, e.g. C1:
 // 100 x 10): all n generations in one launch, a CTA barrier instead of the
@@ -1376,32 +1169,17 @@ cudaError_t launch_eval(int problem, const float* X, long long rows, long long D
     return cudaGetLastError();
 }
 
-// The streaming kernel needs at least U chunks per row segment.
-template <class G>
-static bool use_stream(long long ld) {
-    const bool off = getenv("EVOX_NO_STREAM") != nullptr;  // testing / A-B switch
-    if (U != 4) return false;  // the streaming kernel is written for U == 4
-    const long long NQ = ld >> 2;
-    const long long nseg = (NQ + G::WPR - 1) / G::WPR;
-    return !off && (nseg + G::LPR - 1) / G::LPR >= U;
-}
-
 int pso_gen_grid(int problem, long long ld, long long rows, int device) {
     int g = 1;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
-        const void* fn = use_stream<G_>(ld) ? (const void*)k_pso_gen_stream<P_, G_, true>
-                                            : (const void*)k_pso_gen<P_, G_, true>;
-        g = grid_for(fn, row_units<G_>(rows), device);
+        g = grid_for((const void*)k_pso_gen<P_, G_, true>, row_units<G_>(rows), device);
     }));
     return g;
 }
 
 cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st) {
     EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-        if (use_stream<G_>(a.ld))
-            k_pso_gen_stream<P_, G_, U_><<<grid, 256, 0, st>>>(a);
-        else
-            k_pso_gen<P_, G_, U_><<<grid, 256, 0, st>>>(a);
+        k_pso_gen<P_, G_, U_><<<grid, 256, 0, st>>>(a);
     })));
     return cudaGetLastError();
 }

@@ -182,24 +182,6 @@ def test_pso_small_kernel_equals_grid_kernel(problem, N, D, lb, ub, seed, monkey
     assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
 
 
-@pytest.mark.parametrize("problem,N,D", [("rosenbrock", 300, 100), ("griewank", 257, 200),
-                                         ("ackley", 130, 1000), ("rosenbrock", 40, 4099),
-                                         ("rastrigin", 12, 40001), ("rosenbrock", 70, 30)])
-def test_pso_stream_kernel_equals_group_kernel(problem, N, D, monkeypatch):
-    """The streaming generation kernel (register ring refilled across rows) is bitwise
-    identical to the per-row-group kernel."""
-    lb, ub = WL.BOUNDS[problem]
-    monkeypatch.setenv("EVOX_NO_SMALL", "1")
-    a = ev.PSO(N, D, lb, ub, seed=2)
-    a.step(problem, 7)
-    monkeypatch.setenv("EVOX_NO_STREAM", "1")
-    b = ev.PSO(N, D, lb, ub, seed=2)
-    b.step(problem, 7)
-    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
-    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
-        assert np.array_equal(ga[k], gb[k]), k
-
-
 def test_pso_c1_oneshot_matches_oracle():
     """C1 (PSO/Sphere 100x10, 100 generations, seed 0) in one step(100) call."""
     pso = ev.PSO(100, 10, -5.12, 5.12, seed=0)
