@@ -35,20 +35,21 @@ namespace {
 #ifndef EVOX_MINB
 #define EVOX_MINB 2
 #endif
-constexpr int U = EVOX_U;          // chunks in flight per lane group
+constexpr int U = EVOX_U;          // max chunks in flight per lane group (register slots)
 constexpr int WARPS = 8;           // warps per CTA (256 threads) in every geometry
 constexpr long long MODE_A_MAX = 384;  // quads per warp-iteration prefetched whole (mode A)
 constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
-template <int LPR_, int WPR_>
+template <int LPR_, int WPR_, int U_ = U>
 struct Geom {
     static constexpr int LPR = LPR_;              // lanes per row segment
     static constexpr int WPR = WPR_;              // warps per row
+    static constexpr int NU = U_ < U ? U_ : U;    // chunks in flight per lane group
     static constexpr int RPW = 32 / LPR_;         // rows per warp (WPR == 1)
     static constexpr int RPC = WPR_ == 1 ? WARPS * RPW : WARPS / WPR_;  // rows per CTA pass
-    static constexpr int GROUP = LPR_ * U;        // quads per lane-group iteration
+    static constexpr int GROUP = LPR_ * NU;       // quads per lane-group iteration
 };
 
 // Row segment [qb, qe) of warp `wr` (of WPR) over NQ quads.
@@ -158,12 +159,12 @@ __device__ __forceinline__ void walk_segment(Mover& mv, long long qb, long long 
     for (long long base = qb; base < qe; base += G::GROUP) {
         pf(base);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < G::NU; ++u) {
             const long long q = base + G::LPR * u + sl;
             if (row_ok && q < qe) mv.load(u, q);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < G::NU; ++u) {
             const long long cb = base + G::LPR * u;  // first quad of this chunk
             if (cb >= qe) break;                     // warp-uniform
             const long long q = cb + sl;
@@ -1058,7 +1059,7 @@ int sm_count(int device) {
 using G4 = Geom<4, 1>;
 using G8 = Geom<8, 1>;
 using G32 = Geom<32, 1>;
-using GW8 = Geom<32, 8>;
+using GW8 = Geom<32, 8, 3>;  // long rows: 3 chunks in flight measured best (C5)
 
 // 3: 4 lanes per row (ld <= 128), 0: 8 lanes per row (ld <= 256), 1: a warp per
 // row (ld <= 4096), 2: a CTA per row.  Narrow row groups keep short rows from

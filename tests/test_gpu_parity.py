@@ -450,3 +450,100 @@ def test_cso_c3_sampled():
             O.cso_loser_update_with(X0[w], xl, vl, R1, R2, lb=lb, ub=ub)
             assert np.array_equal(X1[l], xl) and np.array_equal(V1[l], vl)
     assert_fitness(f1[changed][:256], O.evaluate(c.problem, X1[changed][:256]), "C3 f")
+
+
+# ------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("problem,N,D", [("ackley", 40, 37), ("rosenbrock", 33, 101),
+                                         ("griewank", 9, 1003), ("sphere", 5, 4099)])
+def test_pso_per_dimension_bounds(problem, N, D):
+    """Non-uniform bounds take the per-column bounds kernel path (UNI=false)."""
+    lo, hi = WL.BOUNDS[problem]
+    lb = np.linspace(lo, lo / 2, D).astype(np.float32)
+    ub = np.linspace(hi / 3, hi, D).astype(np.float32)
+    pso, log = _run_parity_bounds(problem, N, D, lb, ub, seed=31, gens=12)
+    assert len(log) <= 2, log
+
+
+def _run_parity_bounds(problem, N, D, lb, ub, seed, gens):
+    pso = ev.PSO(N, D, lb, ub, seed=seed)
+    pso.step(problem, 0)
+    st = O.pso_run(problem, N, D, lb, ub, seed=seed, n_gens=0)
+    g = gpu_pso_state(pso, D)
+    compare_pso(g, st, label="t=0")
+    log = []
+    for t in range(1, gens + 1):
+        prev_pf = g["pf"]
+        pso.step(problem, 1)
+        st = O.pso_run(problem, N, D, lb, ub, seed=seed, n_gens=1, state=st)
+        g = gpu_pso_state(pso, D)
+        assert (g["X"] >= lb).all() and (g["X"] <= ub).all()
+        flips = compare_pso(g, st, prev_pf_gpu=prev_pf, label=f"t={t}")
+        if flips:
+            log.append((t, flips))
+            st = resync_oracle_from_gpu(st, g)
+    return pso, log
+
+
+@pytest.mark.parametrize("N,D", [(1, 1), (1, 7), (2, 1), (3, 5), (1, 1000)])
+def test_pso_degenerate_sizes(N, D, monkeypatch):
+    for small in ("0", "1"):
+        if small == "1":
+            monkeypatch.setenv("EVOX_NO_SMALL", "1")
+        pso = ev.PSO(N, D, -2, 2, seed=4)
+        pso.step("rastrigin", 9)
+        st = O.pso_run("rastrigin", N, D, -2, 2, seed=4, n_gens=9)
+        g = gpu_pso_state(pso, D)
+        assert_positions(g["X"], st.X, f"N={N} D={D} X")
+        assert_fitness(g["hist"], np.asarray(st.hist, np.float64), "hist")
+        assert g["gidx"] == st.gidx
+
+
+def test_pso_tell_nan_and_signed_zero():
+    """R-5 through the unfused tell: NaN never improves and ranks as +inf; -0 ranks as +0,
+    ties go to the lowest global index."""
+    pso = ev.PSO(6, 4, -1, 1, seed=0)
+    pso.ask()
+    fit = torch.tensor([float("nan"), 0.0, -0.0, 3.0, float("nan"), -0.0], device="cuda")
+    pso.tell(fit)
+    f, i, row = pso.best()
+    assert f == 0.0 and i == 1
+    X0 = pso.view("X").cpu().numpy()[1, :4]
+    assert np.array_equal(row, X0)
+    pf = pso.view("PF").cpu().numpy()
+    assert np.isinf(pf[0]) and np.isinf(pf[4]) and pf[3] == 3.0
+    pso.ask()
+    pso.tell(torch.full((6,), float("nan"), device="cuda"))
+    f2, i2, _ = pso.best()
+    assert f2 == 0.0 and i2 == 1  # a NaN generation never replaces gbest
+    h = pso.history()
+    assert h[0] == 0.0 and np.isinf(h[1])
+
+
+@pytest.mark.parametrize("N,B,D", [(50, 16, 9), (65, 13, 20), (100, 7, 33), (64, 64, 1001)])
+def test_cso_ragged_blocks(N, B, D):
+    assert _cso_parity("ackley", N, D, B, seed=11, gens=8) <= 1
+
+
+def test_cso_per_dimension_bounds():
+    N, D, B = 64, 21, 16
+    lb = np.linspace(-5.12, -1, D).astype(np.float32)
+    ub = np.linspace(1, 5.12, D).astype(np.float32)
+    cso = ev.CSO(N, D, lb, ub, block=B, seed=6)
+    cso.step("sphere", 5)
+    X, V, f, F64 = O.cso_init("sphere", N, D, lb, ub, 6)
+    for t in range(5):
+        O.cso_generation("sphere", X, V, f, F64, B, t, 6, lb, ub)
+    Xg = cso.view("X").cpu().numpy()[:, :D]
+    assert np.array_equal(Xg, X)
+    assert (Xg >= lb).all() and (Xg <= ub).all()
+
+
+def test_eval_nonfinite_rows():
+    """Non-finite inputs give non-finite fitness; other rows are unaffected."""
+    X = WL.uniform_rows(4, 12, "sphere", 1)
+    X[1, 3] = np.inf
+    X[2, 0] = np.nan
+    f = ev.evaluate("sphere", torch.from_numpy(WL.padded(X)).cuda(), dim=12).cpu().numpy()
+    assert np.isinf(f[1]) and np.isnan(f[2])
+    ref = O.evaluate("sphere", X[[0, 3]])
+    assert_fitness(f[[0, 3]], ref, "finite rows")
