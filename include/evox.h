@@ -48,7 +48,8 @@ typedef enum {
     EVOX_ERR_CUDA = 5,             /* CUDA runtime failure (handle poisoned) */
     EVOX_ERR_NCCL = 6,             /* NCCL failure or NCCL unavailable (handle poisoned) */
     EVOX_ERR_POISONED = 7,         /* handle unusable after an earlier CUDA/NCCL failure */
-    EVOX_ERR_CONFIG = 8            /* configuration error, e.g. CSO block size vs shards */
+    EVOX_ERR_CONFIG = 8,           /* configuration error, e.g. CSO block size vs shards */
+    EVOX_ERR_EXCHANGE = 9          /* peer-memory exchange timed out (a peer stopped; poisoned) */
 } evox_status;
 
 /* Numerical test functions (R-7).  Sphere is the function of the paper's
@@ -81,7 +82,9 @@ typedef struct {
                                 non-blocking stream owned by the handle.  The legacy
                                 default stream (0) is NOT accepted as "NULL" here. */
     const uint8_t* nccl_id;  /* 128-byte ncclUniqueId (from evox_nccl_unique_id on rank 0,
-                                broadcast by the caller) -- required when world > 1 */
+                                broadcast by the caller): world > 1 uses NCCL for the
+                                exchange unless evox_pso_connect() switches the handle to
+                                the in-kernel peer-memory exchange (then it may be NULL) */
     int rank;                /* this process's shard, 0 <= rank < world (SPMD) */
     int world;               /* number of shards/GPUs; 0 or 1: single GPU */
     int device;              /* CUDA device ordinal; -1: the calling thread's current device */
@@ -193,6 +196,30 @@ evox_status evox_pso_sync(evox_pso* s);
 evox_status evox_pso_set_timing(evox_pso* s, int enable);
 evox_status evox_pso_kernel_time(evox_pso* s, double* total_ms, int64_t* gens, int64_t* launches,
                                  int reset);
+
+/* In-kernel peer-memory exchange (the paper's per-
+ * iteration all-gather, fused into the generation kernel).  Every
+ * handle owns a device "mailbox" of 2 x world slots {u64 flag; u64 key;
+ * f32 row[ld]}.  Once connected, the last CTA of each rank's generation
+ * kernel writes its winner record into slot[gen parity][rank] of EVERY rank's
+ * mailbox (NVLink peer stores), release-publishes the flag, waits for the
+ * world records of that generation in its own mailbox, and applies the
+ * strict gbest selection itself -- no NCCL launch, no select kernel.
+ *
+ * evox_pso_mailbox: this handle's mailbox (device pointer and size).
+ * evox_pso_mailbox_ipc: its cudaIpcMemHandle (64 bytes) for other processes.
+ * evox_pso_connect: mode 0 -- `peers` is an array of `world` device pointers
+ *   (the mailboxes of all ranks, same process; GPUs must be peer-capable);
+ *   mode 1 -- `peers` is world x 64 bytes of IPC handles (entry `rank` is
+ *   ignored).  All ranks must connect before any of them steps.  A rank
+ *   that waits more than 60 s (env EVOX_PEER_TIMEOUT_MS at connect time) for
+ *   its peers stops waiting, flags the handle and the next synchronising
+ *   call returns EVOX_ERR_EXCHANGE.  Single-
+ *   process groups must not grow their history during a step (steps that
+ *   would are pre-sized at connect time for 1<<16 generations). */
+evox_status evox_pso_mailbox(evox_pso* s, void** dev, size_t* bytes);
+evox_status evox_pso_mailbox_ipc(evox_pso* s, uint8_t out[64]);
+evox_status evox_pso_connect(evox_pso* s, int mode, const void* peers);
 
 /* Release the handle (never fails for a valid or poisoned handle; NULL ok). */
 evox_status evox_pso_destroy(evox_pso* s);

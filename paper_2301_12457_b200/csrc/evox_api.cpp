@@ -175,8 +175,6 @@ evox_status check_opts(const evox_opts* o, int* world, int* rank) {
     *rank = o->rank;
     if (*rank < 0 || *rank >= *world)
         return fail(EVOX_ERR_INVALID_ARGUMENT, "rank %d out of range for world %d", o->rank, *world);
-    if (*world > 1 && !o->nccl_id)
-        return fail(EVOX_ERR_INVALID_ARGUMENT, "world > 1 requires opts.nccl_id");
     if (o->workspace && ((uintptr_t)o->workspace % kAlign))
         return fail(EVOX_ERR_INVALID_ARGUMENT, "workspace must be %zu-byte aligned", kAlign);
     return EVOX_OK;
@@ -274,6 +272,15 @@ evox_status sync_check(Base* b) {
     DevGuard g(b->device);
     cudaError_t e = cudaStreamSynchronize(b->stream);
     if (e != cudaSuccess) return poison(b, EVOX_ERR_CUDA, "asynchronous CUDA error", e);
+    if (b->ctl) {
+        unsigned int err = 0;
+        e = cudaMemcpy(&err, &b->ctl->err, sizeof err, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return poison(b, EVOX_ERR_CUDA, "reading the control block", e);
+        if (err) {
+            b->poisoned = true;
+            return fail(EVOX_ERR_EXCHANGE, "peer-memory exchange timed out waiting for a peer");
+        }
+    }
     if (b->comm) {
         const evox::NcclApi* api = evox::nccl_api(nullptr);
         ncclResult_t ar = ncclSuccess;
@@ -419,6 +426,14 @@ struct evox_pso : Base {
     unsigned char* rec = nullptr;
     int64_t rec_stride = 0;
     int gen_grid[5] = {0, 0, 0, 0, 0};
+    // in-kernel peer exchange (evox_pso_connect)
+    unsigned char* mbox = nullptr;  // own mailbox (separate cudaMalloc: IPC-exportable)
+    size_t mb_bytes = 0;
+    int64_t mb_slot = 0;
+    bool peer = false;
+    unsigned long long peer_timeout_ns = 60ull * 1000 * 1000 * 1000;
+    unsigned char* peers[evox::kMaxPeers] = {};
+    std::vector<void*> ipc_opened;
     bool asked = false;   // ask issued, tell pending
     int64_t ask_t = 0;    // population index the pending tell refers to
     PsoArgs args() const {
@@ -440,7 +455,11 @@ struct evox_pso : Base {
         a.rec_stride = rec_stride;
         a.rank = rank;
         a.world = world;
-        a.exchange = comm != nullptr;
+        a.exchange = comm != nullptr && !peer;
+        a.peer = peer ? 1 : 0;
+        a.mb_slot = mb_slot;
+        a.peer_timeout_ns = peer_timeout_ns;
+        for (int r = 0; r < evox::kMaxPeers; ++r) a.mbox[r] = peers[r];
         return a;
     }
 };
@@ -471,11 +490,18 @@ evox_status check_pso(evox_pso* s) {
 
 // world > 1: all-gather of the W winner records, then the strict gbest select.
 evox_status pso_exchange(evox_pso* s) {
-    if (!s->comm) return EVOX_OK;
+    if (s->peer || !s->comm) return EVOX_OK;  // peer mode: done inside the kernel
     const evox::NcclApi* api = evox::nccl_api(nullptr);
     NC(s, api->AllGather(s->rec + (int64_t)s->rank * s->rec_stride, s->rec, (size_t)s->rec_stride,
                          ncclUint8, s->comm, s->stream));
     CU(s, evox::launch_gbest_select(s->args(), s->stream));
+    return EVOX_OK;
+}
+
+evox_status check_connected(evox_pso* s) {
+    if (s->world > 1 && !s->comm && !s->peer)
+        return fail(EVOX_ERR_CONTRACT,
+                    "world > 1: pass opts.nccl_id at init or call evox_pso_connect first");
     return EVOX_OK;
 }
 
@@ -592,6 +618,13 @@ evox_status evox_pso_init(int64_t pop, int64_t dim, const float* lb, const float
         DevGuard g(s->device);
         cudaError_t e = evox::launch_pso_init(s->args(), s->stream);
         if (e == cudaSuccess) e = cudaMemsetAsync(s->G, 0, sizeof(float) * s->ld, s->stream);
+        if (e == cudaSuccess && s->world <= evox::kMaxPeers) {
+            // the mailbox of the in-kernel peer exchange (own allocation: IPC-exportable)
+            s->mb_slot = (16 + 4 * s->ld + 15) / 16 * 16;
+            s->mb_bytes = (size_t)(2 * s->world * s->mb_slot);
+            e = cudaMalloc(&s->mbox, s->mb_bytes);
+            if (e == cudaSuccess) e = cudaMemsetAsync(s->mbox, 0, s->mb_bytes, s->stream);
+        }
         if (e != cudaSuccess) st = poison(s, EVOX_ERR_CUDA, "pso init", e);
         for (int p = 0; p < 5 && st == EVOX_OK; ++p)
             s->gen_grid[p] = evox::pso_gen_grid(p, s->ld, s->rows, s->device);
@@ -613,6 +646,8 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
     if (!valid_problem(problem)) return fail(EVOX_ERR_INVALID_ARGUMENT, "unknown problem %d", (int)problem);
     if (n_gens < 0) return fail(EVOX_ERR_INVALID_ARGUMENT, "n_gens must be >= 0");
     if (s->asked) return fail(EVOX_ERR_CONTRACT, "step after ask: tell the pending population first");
+    st = check_connected(s);
+    if (st != EVOX_OK) return st;
     if (s->problem >= 0 && s->problem != (int)problem)
         return fail(EVOX_ERR_CONTRACT, "handle is bound to problem %d (got %d)", s->problem, (int)problem);
     if (n_gens > (int64_t)0xFFFFFFFFll - 2 - s->t)
@@ -629,7 +664,7 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
     const PsoArgs a = s->args();
     const int grid = s->gen_grid[problem];
     const bool no_small = std::getenv("EVOX_NO_SMALL") != nullptr;  // testing: force multi-CTA
-    if (!s->comm && !no_small && evox::pso_small(s->rows, s->ld)) {
+    if (!s->comm && !s->peer && !no_small && evox::pso_small(s->rows, s->ld)) {
         CU(s, timed(s, [&] { return evox::launch_pso_run_small((int)problem, a, n_gens, s->stream); },
                     n_gens));
         s->t += n_gens;
@@ -649,6 +684,8 @@ evox_status evox_pso_ask(evox_pso* s, const float** X_dev, int64_t* rows, int64_
     if (st != EVOX_OK) return st;
     if (!X_dev) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL X_dev");
     if (s->asked) return fail(EVOX_ERR_CONTRACT, "ask twice without tell");
+    st = check_connected(s);
+    if (st != EVOX_OK) return st;
     DevGuard g(s->device);
     if (s->t < 0) {
         s->ask_t = 0;  // first ask: X0, unmoved
@@ -845,6 +882,78 @@ evox_status evox_pso_load(evox_pso* s, const void* host_blob, size_t size) {
     return EVOX_OK;
 }
 
+evox_status evox_pso_mailbox(evox_pso* s, void** dev, size_t* bytes) {
+    evox_status st = check_pso(s);
+    if (st != EVOX_OK) return st;
+    if (!s->mbox) return fail(EVOX_ERR_CONFIG, "no mailbox (world > %d)", evox::kMaxPeers);
+    if (dev) *dev = s->mbox;
+    if (bytes) *bytes = s->mb_bytes;
+    return EVOX_OK;
+}
+
+evox_status evox_pso_mailbox_ipc(evox_pso* s, uint8_t out[64]) {
+    evox_status st = check_pso(s);
+    if (st != EVOX_OK) return st;
+    if (!out) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL output");
+    if (!s->mbox) return fail(EVOX_ERR_CONFIG, "no mailbox (world > %d)", evox::kMaxPeers);
+    DevGuard g(s->device);
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+    CU(s, cudaIpcGetMemHandle(&h, s->mbox));
+    std::memcpy(out, &h, 64);
+    return EVOX_OK;
+}
+
+evox_status evox_pso_connect(evox_pso* s, int mode, const void* peers) {
+    evox_status st = check_pso(s);
+    if (st != EVOX_OK) return st;
+    if (!peers) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL peers");
+    if (mode != 0 && mode != 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
+    if (!s->mbox) return fail(EVOX_ERR_CONFIG, "peer exchange supports world <= %d", evox::kMaxPeers);
+    if (s->t >= 0 || s->asked) return fail(EVOX_ERR_CONTRACT, "connect before the first step/ask");
+    DevGuard g(s->device);
+    for (int r = 0; r < s->world; ++r) {
+        if (r == s->rank) {
+            s->peers[r] = s->mbox;
+            continue;
+        }
+        if (mode == 0) {
+            void* p = static_cast<void* const*>(peers)[r];
+            if (!p) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL mailbox pointer for rank %d", r);
+            cudaPointerAttributes at;
+            CU(s, cudaPointerGetAttributes(&at, p));
+            if (at.device != s->device) {
+                int can = 0;
+                CU(s, cudaDeviceCanAccessPeer(&can, s->device, at.device));
+                if (!can)
+                    return fail(EVOX_ERR_CONFIG, "device %d cannot access device %d", s->device,
+                                at.device);
+                cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else if (e != cudaSuccess) return poison(s, EVOX_ERR_CUDA, "cudaDeviceEnablePeerAccess", e);
+            }
+            s->peers[r] = static_cast<unsigned char*>(p);
+        } else {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const uint8_t*>(peers) + 64 * r, 64);
+            void* p = nullptr;
+            CU(s, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            s->ipc_opened.push_back(p);
+            s->peers[r] = static_cast<unsigned char*>(p);
+        }
+    }
+    // a step must never synchronise (single-process groups would deadlock):
+    // pre-size the history
+    st = ensure_hist(s, 1 << 16);
+    if (st != EVOX_OK) return st;
+    if (const char* ms = std::getenv("EVOX_PEER_TIMEOUT_MS"))  // tests shorten the 60 s default
+        s->peer_timeout_ns = (unsigned long long)std::strtoull(ms, nullptr, 10) * 1000000ull;
+    s->peer = true;
+    for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);  // args changed
+    s->graphs.clear();
+    return EVOX_OK;
+}
+
 evox_status evox_pso_set_timing(evox_pso* s, int enable) {
     evox_status st = check_pso(s);
     if (st != EVOX_OK) return st;
@@ -873,6 +982,13 @@ evox_status evox_pso_kernel_time(evox_pso* s, double* total_ms, int64_t* gens, i
 
 evox_status evox_pso_destroy(evox_pso* s) {
     if (!s) return EVOX_OK;
+    {
+        DevGuard g(s->device);
+        if (s->stream) cudaStreamSynchronize(s->stream);
+        for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
+        if (s->mbox) cudaFree(s->mbox);
+        cudaGetLastError();
+    }
     base_release(s);
     delete s;
     return EVOX_OK;

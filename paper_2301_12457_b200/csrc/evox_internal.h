@@ -9,16 +9,18 @@
 
 namespace evox {
 
+constexpr int kMaxPeers = 8;  // ranks reachable by the in-kernel peer exchange
+
 // Device-resident control block of a handle.  Kernels read the generation
 // index from here (not from launch parameters) so one captured CUDA graph can
 // be replayed for any generation.
 struct Ctl {
     unsigned long long gen_key;  // atomicMin accumulator of the running generation (~0 at rest)
     unsigned int ticket;         // CTAs finished in the running kernel (0 at rest)
-    unsigned int phase;          // unused by kernels
+    unsigned int err;            // 1: peer exchange timed out (checked by the host at sync)
     unsigned long long t;        // index of the current population
     float gf;                    // best-so-far fitness (PSO) / scratch
-    int pad;
+    int pad;                     // unused
     long long gidx;              // global row of gbest (-1: none)
     float* hist;                 // hist[t] = min f of generation t
     unsigned long long* hkeys;   // CSO, world > 1: per-generation local min keys
@@ -48,6 +50,10 @@ struct PsoArgs {
     long long rec_stride;
     int rank, world;
     int exchange;  // 1: publish the local winner record for the NCCL exchange (A13)
+    int peer;      // 1: in-kernel peer-memory exchange through the mailboxes
+    long long mb_slot;            // bytes per mailbox slot (16 + 4 ld, 16-aligned)
+    unsigned long long peer_timeout_ns;
+    unsigned char* mbox[kMaxPeers];  // every rank's mailbox (own included)
 };
 
 struct CsoArgs {

@@ -400,6 +400,89 @@ __device__ __forceinline__ bool grid_argmin(Ctl* ctl, unsigned long long my_key,
     return true;
 }
 
+// Peer-memory exchange primitives (system scope: the mailboxes of other ranks
+// are NVLink peer memory mapped into this address space).
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// The last CTA's winner record -> every rank's mailbox slot[par][rank]; wait for
+// the world records of this generation; strict gbest selection (A13, fused).
+// Every rank selects from the same world records: identical G on all ranks.
+__device__ void peer_exchange(const PsoArgs& a, unsigned long long key, unsigned long long t_new) {
+    __shared__ int sh_w, sh_better;
+    __shared__ unsigned long long sh_key;
+    Ctl* ctl = a.ctl;
+    const long long NQ = a.ld >> 2;
+    const int par = (int)(t_new & 1);
+    const unsigned long long flag = t_new + 1;  // mailboxes start zeroed: 0 = nothing yet
+    const bool any = key != ~0ull;
+    const long long grow = (long long)(uint32_t)(key & 0xffffffffu);
+    const float4* src = reinterpret_cast<const float4*>(a.X + (any ? grow - a.row0 : 0) * a.ld);
+    const long long my_off = ((long long)par * a.world + a.rank) * a.mb_slot;
+    for (long long q = threadIdx.x; q < NQ; q += blockDim.x) {
+        const float4 v = any ? __ldcg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int p = 0; p < a.world; ++p)
+            reinterpret_cast<float4*>(a.mbox[p] + my_off + 16)[q] = v;
+    }
+    if (threadIdx.x == 0)
+        for (int p = 0; p < a.world; ++p)
+            *reinterpret_cast<unsigned long long*>(a.mbox[p] + my_off + 8) = key;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int p = 0; p < a.world; ++p)
+            st_release_sys(reinterpret_cast<unsigned long long*>(a.mbox[p] + my_off), flag);
+        // wait for every rank's record of this generation in our own mailbox
+        const unsigned long long t0 = globaltimer_ns();
+        unsigned long long kmin = ~0ull;
+        int w = -1;
+        for (int r = 0; r < a.world; ++r) {
+            const unsigned char* slot = a.mbox[a.rank] + ((long long)par * a.world + r) * a.mb_slot;
+            while (ld_acquire_sys(reinterpret_cast<const unsigned long long*>(slot)) != flag) {
+                if (globaltimer_ns() - t0 > a.peer_timeout_ns) {
+                    ctl->err = 1;
+                    break;
+                }
+                __nanosleep(256);
+            }
+            const unsigned long long kr = __ldcg(reinterpret_cast<const unsigned long long*>(slot + 8));
+            if (kr < kmin) { kmin = kr; w = r; }
+        }
+        const bool ok = kmin != ~0ull;
+        const float fmin = ok ? unord_f32((uint32_t)(kmin >> 32)) : __int_as_float(0x7f800000);
+        sh_key = kmin;
+        sh_w = w;
+        sh_better = ok && fmin < ctl->gf;  // strict improvement (R-5)
+    }
+    __syncthreads();
+    if (sh_better) {
+        const float4* wr = reinterpret_cast<const float4*>(
+            a.mbox[a.rank] + ((long long)par * a.world + sh_w) * a.mb_slot + 16);
+        float4* G = reinterpret_cast<float4*>(a.G);
+        for (long long q = threadIdx.x; q < NQ; q += blockDim.x) G[q] = __ldcg(wr + q);
+    }
+    if (threadIdx.x == 0) {
+        const unsigned long long k = sh_key;
+        const float fmin = k != ~0ull ? unord_f32((uint32_t)(k >> 32)) : __int_as_float(0x7f800000);
+        if (sh_better) {
+            ctl->gf = fmin;
+            ctl->gidx = (long long)(uint32_t)(k & 0xffffffffu);
+        }
+        ctl->hist[t_new] = fmin;
+    }
+}
+
 // In the last CTA: gbest update (strict, R-5), hist, or the winner record for
 // the exchange.  `t_new` is the index of the population just evaluated.
 __device__ void pso_finalize(const PsoArgs& a, unsigned long long key, unsigned long long t_new) {
@@ -408,7 +491,9 @@ __device__ void pso_finalize(const PsoArgs& a, unsigned long long key, unsigned 
     const bool any = key != ~0ull;
     const long long grow = (long long)(uint32_t)(key & 0xffffffffu);
     const float fmin = any ? unord_f32((uint32_t)(key >> 32)) : __int_as_float(0x7f800000);
-    if (a.exchange) {
+    if (a.peer) {
+        peer_exchange(a, key, t_new);
+    } else if (a.exchange) {
         // winner record {u64 key; u32 pad[2]; f32 row[ld]} into this rank's slot
         unsigned char* rec = a.rec + (long long)a.rank * a.rec_stride;
         const float4* src = reinterpret_cast<const float4*>(a.X + (any ? grow - a.row0 : 0) * a.ld);

@@ -27,7 +27,8 @@ DEFAULT_BOUNDS = {"sphere": (-5.12, 5.12), "ackley": (-32.768, 32.768),
                   "rosenbrock": (-5.0, 10.0)}
 FIELDS = {"X": 0, "V": 1, "P": 2, "F": 3, "PF": 4, "G": 5}
 
-OK, INVALID_ARGUMENT, SHAPE, CONTRACT, OUT_OF_MEMORY, CUDA, NCCL, POISONED, CONFIG = range(9)
+OK, INVALID_ARGUMENT, SHAPE, CONTRACT, OUT_OF_MEMORY, CUDA, NCCL, POISONED, CONFIG, EXCHANGE = \
+    range(10)
 
 
 class EvoxError(RuntimeError):
@@ -44,11 +45,12 @@ class CudaError(EvoxError): pass
 class NcclError(EvoxError): pass
 class PoisonedError(EvoxError): pass
 class ConfigError(EvoxError, ValueError): pass
+class ExchangeError(EvoxError): pass
 
 
 _EXC = {INVALID_ARGUMENT: InvalidArgument, SHAPE: ShapeError, CONTRACT: ContractError,
         OUT_OF_MEMORY: OutOfMemory, CUDA: CudaError, NCCL: NcclError, POISONED: PoisonedError,
-        CONFIG: ConfigError}
+        CONFIG: ConfigError, EXCHANGE: ExchangeError}
 
 
 class EvoxOpts(ctypes.Structure):
@@ -85,6 +87,9 @@ SIGNATURES = {
     "evox_pso_sync": ([_p], _i),
     "evox_pso_destroy": ([_p], _i),
     "evox_pso_set_timing": ([_p, _i], _i),
+    "evox_pso_mailbox": ([_p, _PP, _PSZ], _i),
+    "evox_pso_mailbox_ipc": ([_p, _p], _i),
+    "evox_pso_connect": ([_p, _i, _p], _i),
     "evox_pso_kernel_time": ([_p, ctypes.POINTER(ctypes.c_double), _PI64, _PI64, _i], _i),
     "evox_cso_workspace_bytes": ([_i64, _i64, _i, _i, _PSZ], _i),
     "evox_cso_init": ([_i64, _i64, _p, _p, _f32, _i64, _u64, _p, _PP], _i),
@@ -370,6 +375,27 @@ class PSO(_Handle):
         _check(lib().evox_pso_ask(self._h, ctypes.byref(ptr), ctypes.byref(rows),
                                   ctypes.byref(ld)))
         return _as_tensor(ptr.value, (rows.value, ld.value), "<f4", self, self.device)
+
+    # ---- in-kernel peer-memory exchange (NEXT #1)
+    def mailbox(self) -> tuple[int, int]:
+        ptr, n = ctypes.c_void_p(), ctypes.c_size_t()
+        _check(lib().evox_pso_mailbox(self._h, ctypes.byref(ptr), ctypes.byref(n)))
+        return ptr.value, n.value
+
+    def mailbox_ipc(self) -> bytes:
+        buf = (ctypes.c_uint8 * 64)()
+        _check(lib().evox_pso_mailbox_ipc(self._h, buf))
+        return bytes(buf)
+
+    def connect_local(self, mailboxes):
+        """Same-process group: `mailboxes` = [PSO.mailbox()[0] of rank r for r in range(world)]."""
+        arr = (ctypes.c_void_p * len(mailboxes))(*[int(m) for m in mailboxes])
+        _check(lib().evox_pso_connect(self._h, 0, arr))
+
+    def connect_ipc(self, handles):
+        """Multi-process group: `handles` = [64-byte PSO.mailbox_ipc() of rank r]."""
+        buf = ctypes.create_string_buffer(b"".join(bytes(h) for h in handles))
+        _check(lib().evox_pso_connect(self._h, 1, buf))
 
     def tell(self, fitness):
         """Algorithm.tell with a [rows] float32 CUDA tensor of this rank's fitness."""
