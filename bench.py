@@ -213,6 +213,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--pop", type=int, default=0, help="override the population (profiling only)")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="PSO winner exchange for N>1: in-kernel over NVLink peer memory "
+                         "(default) or NCCL all-gather + select kernel")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = WL.CONFIGS[args.config]
@@ -236,7 +239,8 @@ def main():
     if launched:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nid = None
-    if world > 1:
+    peer = world > 1 and cfg.algo == "pso" and args.exchange == "peer"
+    if world > 1 and not peer:
         buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
             buf.copy_(torch.frombuffer(bytearray(ev.nccl_unique_id()), dtype=torch.uint8))
@@ -252,6 +256,12 @@ def main():
     Cls = ev.PSO if cfg.algo == "pso" else ev.CSO
     kw = {} if cfg.algo == "pso" else {"block": cfg.pop // 8 if cfg.pop % 16 == 0 else 0}
     h = Cls(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world, nccl_id=nid, **kw)
+    if peer:  # mailboxes of all ranks mapped into every rank through CUDA IPC
+        mine = torch.frombuffer(bytearray(h.mailbox_ipc()), dtype=torch.uint8).cuda()
+        allh = [torch.zeros(64, dtype=torch.uint8, device="cuda") for _ in range(world)]
+        dist.all_gather(allh, mine)
+        h.connect_ipc([bytes(x.cpu().numpy().tobytes()) for x in allh])
+        barrier()
     rows = h.info()["rows"]
     stream = h.stream
     h.step(cfg.problem, 0)          # generation 0: evaluate X0 + tell
@@ -316,7 +326,9 @@ def main():
             "data": "synthetic",
             "config": {"workload": cfg.note, "algo": cfg.algo, "problem": cfg.problem,
                        "pop": cfg.pop, "dim": cfg.dim, "seed": 0,
-                       "parallelism": f"row-sharded x{world}",
+                       "parallelism": f"row-sharded x{world}" + (
+                           f", exchange={'peer-memory (in-kernel)' if peer else 'nccl'}"
+                           if world > 1 else ""),
                        "l2": "state (X,V,P) > L2: inputs larger than L2, no flush needed"
                        if 12 * cfg.pop * cfg.dim > 2 * 126e6 else "state comparable to L2"},
             "individual_dims_per_s": gens_per_s * evaluated,
@@ -328,7 +340,8 @@ def main():
                          "peak_source": peak_src},
             "clocks": clk,
             # generation kernels timed by the library (+ the gbest select per step when W > 1)
-            "gpu_launches": k_launch + (args.steps if (cfg.algo == "pso" and world > 1) else 0),
+            "gpu_launches": k_launch + (args.steps if (cfg.algo == "pso" and world > 1
+                                                       and not peer) else 0),
             "e2e": {"value": args.e2e_steps / e2e_s, "unit": "generations/s",
                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 + 8 + 4 * cfg.dim,
                     "note": "per step: evox_*_step(1) through the C-ABI + synchronising "

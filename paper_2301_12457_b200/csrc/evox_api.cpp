@@ -216,7 +216,8 @@ evox_status base_setup(Base* b, int64_t pop, int64_t dim, const float* lb, const
     // EVOX_FORCE_NCCL=1 runs a single-GPU handle through the NCCL exchange path
     // (a 1-rank communicator) so the multi-GPU code is exercised on one GPU.
     const char* force = std::getenv("EVOX_FORCE_NCCL");
-    if (world > 1 || (force && *force == '1')) {
+    // world > 1 without a unique id: the caller will evox_pso_connect() the peers
+    if ((world > 1 && o && o->nccl_id) || (world == 1 && force && *force == '1')) {
         const char* why = "";
         const evox::NcclApi* api = evox::nccl_api(&why);
         if (!api) return fail(EVOX_ERR_NCCL, "NCCL unavailable: %s", why);
