@@ -234,14 +234,23 @@ def main():
 
     import paper_2301_12457_b200 as ev
 
+    # EVOX_BENCH_SAME_GPU=1: every rank on cuda:0 with a gloo group -- validates the N>1 flow
+    # (IPC mailboxes, barriers, max-over-ranks) on a 1-GPU box; its timings are meaningless.
+    same_gpu = os.environ.get("EVOX_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     launched = "WORLD_SIZE" in os.environ  # under torchrun: use the process group even at N=1
+    cdev = "cpu" if same_gpu else "cuda"   # device of the collective tensors
     if launched:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nid = None
     peer = world > 1 and cfg.algo == "pso" and args.exchange == "peer"
     if world > 1 and not peer:
-        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        buf = torch.zeros(128, dtype=torch.uint8, device=cdev)
         if rank == 0:
             buf.copy_(torch.frombuffer(bytearray(ev.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(buf, 0)
@@ -257,8 +266,8 @@ def main():
     kw = {} if cfg.algo == "pso" else {"block": cfg.pop // 8 if cfg.pop % 16 == 0 else 0}
     h = Cls(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world, nccl_id=nid, **kw)
     if peer:  # mailboxes of all ranks mapped into every rank through CUDA IPC
-        mine = torch.frombuffer(bytearray(h.mailbox_ipc()), dtype=torch.uint8).cuda()
-        allh = [torch.zeros(64, dtype=torch.uint8, device="cuda") for _ in range(world)]
+        mine = torch.frombuffer(bytearray(h.mailbox_ipc()), dtype=torch.uint8).to(cdev)
+        allh = [torch.zeros(64, dtype=torch.uint8, device=cdev) for _ in range(world)]
         dist.all_gather(allh, mine)
         h.connect_ipc([bytes(x.cpu().numpy().tobytes()) for x in allh])
         barrier()
@@ -285,7 +294,7 @@ def main():
     k_ms, k_n, k_launch = h.kernel_time(reset=True)
     h.set_timing(False)
     # one launch of the persistent small-population kernel runs all the steps
-    t = torch.tensor([ms_local, k_ms / max(k_n, 1)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms_local, k_ms / max(k_n, 1)], dtype=torch.float64, device=cdev)
     if launched:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total, k_avg_ms = float(t[0]), float(t[1])
@@ -299,7 +308,7 @@ def main():
         h.step(cfg.problem, 1)
         best = h.best(with_row=True)  # synchronising D2H: fitness, index, best row
     e2e_s = time.perf_counter() - t0
-    e2e = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    e2e = torch.tensor([e2e_s], dtype=torch.float64, device=cdev)
     if launched:
         dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     e2e_s = float(e2e[0])
