@@ -95,8 +95,16 @@ __device__ __forceinline__ unsigned long long make_key(float f, long long global
 // Streaming (evict-first) loads/stores for the population: each element is
 // touched once per generation and the state (12 GB at the headline config)
 // is far larger than L2, so keep L2 for G, bounds, f/pf/imp.
+#ifndef EVOX_EF
+#define EVOX_EF 1
+#endif
+#if EVOX_EF
 __device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
+#else  // tuning variant: default cache policy (lets an L2-sized state stay resident)
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return *p; }
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { *p = v; }
+#endif
 
 // --------------------------------------------------------- fitness (R-7)
 // fp32 forms that are algebraically identical to the textbook definitions
