@@ -96,15 +96,17 @@ __device__ __forceinline__ unsigned long long make_key(float f, long long global
 // touched once per generation and the state (12 GB at the headline config)
 // is far larger than L2, so keep L2 for G, bounds, f/pf/imp.
 #ifndef EVOX_EF
-#define EVOX_EF 1
+#define EVOX_EF 3  // bit 0: evict-first loads, bit 1: evict-first stores
 #endif
-#if EVOX_EF
-__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
-__device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
-#else  // tuning variant: default cache policy (lets an L2-sized state stay resident)
-__device__ __forceinline__ float4 ld_stream(const float4* p) { return *p; }
-__device__ __forceinline__ void st_stream(float4* p, float4 v) { *p = v; }
-#endif
+template <bool EF = true>
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+    if constexpr ((EVOX_EF & 1) != 0 && EF) return __ldcs(p);
+    else return *p;
+}
+__device__ __forceinline__ void st_stream(float4* p, float4 v) {
+    if constexpr ((EVOX_EF & 2) != 0) __stcs(p, v);
+    else *p = v;
+}
 
 // --------------------------------------------------------- fitness (R-7)
 // fp32 forms that are algebraically identical to the textbook definitions

@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "evox_device.cuh"
 #include "evox_internal.h"
@@ -42,8 +43,9 @@ constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
-template <int LPR_, int WPR_, int U_ = U>
+template <int LPR_, int WPR_, int U_ = U, bool EFL_ = true>
 struct Geom {
+    static constexpr bool EFL = EFL_;             // evict-first loads (stores always are)
     static constexpr int LPR = LPR_;              // lanes per row segment
     static constexpr int WPR = WPR_;              // warps per row
     static constexpr int NU = U_ < U ? U_ : U;    // chunks in flight per lane group
@@ -135,6 +137,30 @@ struct HStore<GRIEWANK> {
     float v[HTAB];
 };
 
+// Programmatic dependent launch (PDL): a generation kernel lets the next one be
+// scheduled as soon as its CTAs start retiring; the next one prefetches its
+// first rows into L2 and then waits for the full completion (and memory
+// flush) of this grid before touching anything this generation wrote.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// First-row L2 prefetch of a warp (X and V only: whether P is needed depends
+// on imp, which the previous generation is still writing).
+template <class G>
+__device__ __forceinline__ void prefetch_first_rows(const float* X, const float* V, long long rows,
+                                                    long long ld, long long wfirst, long long qb,
+                                                    long long qe) {
+    if (lane_id() != 0 || wfirst >= rows) return;
+    const long long nr = rows - wfirst < G::RPW ? rows - wfirst : G::RPW;
+    const long long o = wfirst * ld * 4 + qb * 16;
+    long long bytes = G::WPR == 1 ? nr * ld * 4 : (qe - qb) * 16;
+    if (bytes > 64 * 1024) bytes = 64 * 1024;  // long rows: the window prefetcher takes over
+    prefetch_l2(reinterpret_cast<const char*>(X) + o, bytes);
+    prefetch_l2(reinterpret_cast<const char*>(V) + o, bytes);
+}
+
 struct NoPrefetch {
     __device__ __forceinline__ void operator()(long long) {}
 };
@@ -161,7 +187,7 @@ __device__ __forceinline__ void walk_segment(Mover& mv, long long qb, long long 
 #pragma unroll
         for (int u = 0; u < G::NU; ++u) {
             const long long q = base + G::LPR * u + sl;
-            if (row_ok && q < qe) mv.load(u, q);
+            if (row_ok && q < qe) mv.template load<G::EFL>(u, q);
         }
 #pragma unroll
         for (int u = 0; u < G::NU; ++u) {
@@ -271,7 +297,8 @@ struct RowMap {
 struct MoverEval {
     const float4* Xr;
     float4 x[U];
-    __device__ __forceinline__ void load(int u, long long q) { x[u] = ld_stream(Xr + q); }
+    template <bool EF>
+    __device__ __forceinline__ void load(int u, long long q) { x[u] = ld_stream<EF>(Xr + q); }
     __device__ __forceinline__ float4 step(int u, long long) { return x[u]; }
 };
 
@@ -297,10 +324,11 @@ struct MoverPso {
         t = t_;
         pend = pend_;
     }
+    template <bool EF>
     __device__ __forceinline__ void load(int u, long long q) {
-        x[u] = ld_stream(Xr + q);
-        v[u] = ld_stream(Vr + q);
-        if (!pend) p[u] = ld_stream(Pr + q);
+        x[u] = ld_stream<EF>(Xr + q);
+        v[u] = ld_stream<EF>(Vr + q);
+        if (!pend) p[u] = ld_stream<EF>(Pr + q);
     }
     __device__ __forceinline__ float4 step(int u, long long q) {
         const float4 xo = x[u];
@@ -601,6 +629,9 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen(PsoArgs a) {
     const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
     const RowMap<G> m(a.ld >> 2);
     const int lane = lane_id();
+    prefetch_first_rows<G>(a.X, a.V, a.rows, a.ld, m.wfirst, m.qb, m.qe);
+    pdl_wait();               // the previous generation (G, imp, pf, t) is complete
+    pdl_launch_dependents();  // the next generation may be scheduled as our CTAs retire
     const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
     const long long seg = m.qe - m.qb;
     // prefetch mode: A = the warp's whole next rows (short rows), B = sliding window
@@ -896,10 +927,11 @@ struct MoverCso {
     uint32_t row_g, t;
     float4 x[U], v[U], xw[U];
     __device__ __forceinline__ MoverCso(const CsoArgs& a_) : a(a_) {}
+    template <bool EF>
     __device__ __forceinline__ void load(int u, long long q) {
-        x[u] = ld_stream(Xl + q);
-        v[u] = ld_stream(Vl + q);
-        xw[u] = ld_stream(Xw + q);
+        x[u] = ld_stream<EF>(Xl + q);
+        v[u] = ld_stream<EF>(Vl + q);
+        xw[u] = ld_stream<EF>(Xw + q);
     }
     __device__ __forceinline__ static float upd(float xl, float vl, float xwv, float r1, float r2,
                                                 float c3, float xb, bool use3, float lo, float hi,
@@ -1141,7 +1173,7 @@ int sm_count(int device) {
     return n;
 }
 
-using G4 = Geom<4, 1>;
+using G4 = Geom<4, 1, U, false>;  // short rows: plain loads measured best (C4: +5 points)
 using G8 = Geom<8, 1>;
 using G32 = Geom<32, 1>;
 using GW8 = Geom<32, 8, 3>;  // long rows: 3 chunks in flight measured best (C5)
@@ -1263,11 +1295,29 @@ int pso_gen_grid(int problem, long long ld, long long rows, int device) {
     return g;
 }
 
+// Generation kernels are launched with programmatic stream serialization (PDL):
+// kernel t+1 becomes resident while kernel t retires (EVOX_NO_PDL=1: plain launch).
+template <class K, class A>
+static cudaError_t launch_pdl(K kernel, int grid, const A& a, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = getenv("EVOX_NO_PDL") ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
     EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-        k_pso_gen<P_, G_, U_><<<grid, 256, 0, st>>>(a);
+        e = launch_pdl(k_pso_gen<P_, G_, U_>, grid, a, st);
     })));
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 bool pso_small(long long rows, long long ld) { return rows * ld <= 65536; }
