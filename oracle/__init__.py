@@ -75,6 +75,11 @@ def lib() -> ctypes.CDLL:
         L.oracle_cso_loser_update_with.argtypes = [i64, P, P, P, P, P, P, f32, P, P, P]
         L.oracle_cso_generation.argtypes = [i32, i64, i64, i64, u64, u64, f32, P, P, P, P, P, P,
                                             i32]
+        L.oracle_de_indices.argtypes = [i64, i64, u64, u64, P]
+        L.oracle_de_jrand.argtypes = [i64, i64, u64, u64]
+        L.oracle_de_jrand.restype = i64
+        L.oracle_de_trial_with.argtypes = [i64, P, P, P, P, P, i64, f32, f32, P, P, P]
+        L.oracle_de_generation.argtypes = [i32, i64, i64, P, P, P, f32, f32, u64, u64, P, P, i32]
         _lib = L
     return _lib
 
@@ -266,3 +271,41 @@ def cso_generation(problem, X, V, f, F64, B, t, seed, lb, ub, phi=0.0, threads=1
     lb, ub = _bounds(lb, ub, D)
     lib().oracle_cso_generation(int(problem), N, D, B, t, seed, phi, _p(lb), _p(ub), _p(X),
                                 _p(V), _p(f), _p(F64), threads)
+
+
+# --------------------------------------------------------------------- DE
+def de_indices(N, i, t, seed) -> list:
+    out = np.zeros(3, np.int64)
+    lib().oracle_de_indices(N, i, t, seed, _p(out))
+    return [int(v) for v in out]
+
+
+def de_jrand(D, i, t, seed) -> int:
+    return int(lib().oracle_de_jrand(D, i, t, seed))
+
+
+def de_trial_with(xi, xa, xb, xc, U, jrand, F, CR, lb=-np.inf, ub=np.inf):
+    """DE/rand/1/bin trial with injected crossover uniforms (hand-worked example hook)."""
+    D = len(xi)
+    lb, ub = _bounds(lb, ub, D)
+    u = np.zeros(D, np.float32)
+    lib().oracle_de_trial_with(D, _p(_f32(xi)), _p(_f32(xa)), _p(_f32(xb)), _p(_f32(xc)),
+                               _p(_f32(np.broadcast_to(U, (D,)))), jrand, F, CR, _p(lb), _p(ub),
+                               _p(u))
+    return u
+
+
+def de_init(problem, N, D, lb, ub, seed, threads=1):
+    """DE init (R-14): X0 as PSO init (tag 0), evaluate all rows."""
+    X, _ = pso_init(N, D, 0, lb, ub, seed)
+    F64 = evaluate(problem, X, threads)
+    return X, F64.astype(np.float32), F64
+
+
+def de_generation(problem, X, f, F64, t, seed, lb, ub, F=0.5, CR=0.9, threads=1):
+    """One synchronous DE generation at t, in place."""
+    problem = PROBLEMS.get(problem, problem)
+    N, D = X.shape
+    lb, ub = _bounds(lb, ub, D)
+    lib().oracle_de_generation(int(problem), N, D, _p(X), _p(f), _p(F64), F, CR, t, seed, _p(lb),
+                               _p(ub), threads)

@@ -415,3 +415,86 @@ void oracle_cso_generation(int problem, int64_t N, int64_t D, int64_t B, uint64_
     }
     free(xbar);
 }
+
+/* ------------------------------------------------------------------- DE */
+/* Donor indices (R-14): rejection sampling on a counter-based word stream. */
+void oracle_de_indices(int64_t N, int64_t i, uint64_t t, uint64_t seed, int64_t out[3]) {
+    uint32_t key[2], ctr[4], w[4];
+    int64_t got = 0;
+    uint32_t c = 0;
+    key_of(seed, key);
+    while (got < 3) {
+        int l;
+        ctr[0] = c++;
+        ctr[1] = (uint32_t)i;
+        ctr[2] = (uint32_t)t;
+        ctr[3] = 8;
+        oracle_philox4x32_10(ctr, key, w);
+        for (l = 0; l < 4 && got < 3; ++l) {
+            int64_t r = (int64_t)(((uint64_t)w[l] * (uint64_t)N) >> 32);
+            int ok = r != i, k;
+            for (k = 0; k < got; ++k) ok = ok && r != out[k];
+            if (ok) out[got++] = r;
+        }
+    }
+}
+
+int64_t oracle_de_jrand(int64_t D, int64_t i, uint64_t t, uint64_t seed) {
+    uint32_t key[2], ctr[4], w[4];
+    key_of(seed, key);
+    ctr[0] = 0;
+    ctr[1] = (uint32_t)i;
+    ctr[2] = (uint32_t)t;
+    ctr[3] = 9;
+    oracle_philox4x32_10(ctr, key, w);
+    return (int64_t)(((uint64_t)w[0] * (uint64_t)D) >> 32);
+}
+
+/* Mutation v = x_a + F (x_b - x_c) and binomial crossover. */
+void oracle_de_trial_with(int64_t D, const float* xi, const float* xa, const float* xb,
+                          const float* xc, const float* U, int64_t jrand, float F, float CR,
+                          const float* lb, const float* ub, float* u) {
+    int64_t j;
+    for (j = 0; j < D; ++j) {
+        float v = fmaf(F, xb[j] - xc[j], xa[j]);
+        float y = (U[j] < CR || j == jrand) ? v : xi[j];
+        u[j] = fminf(fmaxf(y, lb[j]), ub[j]);
+    }
+}
+
+static float nan_as_inf(float v) { return isnan(v) ? INFINITY : v; }
+
+/* One-to-one greedy replacement, "trial replaces target iff trial fitness <=
+ * target fitness", synchronous over the population. */
+void oracle_de_generation(int problem, int64_t N, int64_t D, float* X, float* f, double* F64,
+                          float F, float CR, uint64_t t, uint64_t seed, const float* lb,
+                          const float* ub, int threads) {
+    float* T = (float*)malloc(sizeof(float) * (size_t)(N * D > 0 ? N * D : 1));
+    double* FT = (double*)malloc(sizeof(double) * (size_t)(N > 0 ? N : 1));
+    int64_t i;
+    set_threads(threads);
+#pragma omp parallel for schedule(static)
+    for (i = 0; i < N; ++i) {
+        uint32_t key[2];
+        int64_t r[3], j, jr;
+        float* U = (float*)malloc(sizeof(float) * (size_t)(D > 0 ? D : 1));
+        key_of(seed, key);
+        oracle_de_indices(N, i, t, seed, r);
+        jr = oracle_de_jrand(D, i, t, seed);
+        for (j = 0; j < D; ++j) U[j] = draw_one(j, i, t, 10, key);
+        oracle_de_trial_with(D, X + i * D, X + r[0] * D, X + r[1] * D, X + r[2] * D, U, jr, F, CR,
+                             lb, ub, T + i * D);
+        FT[i] = eval_row(problem, D, T + i * D);
+        free(U);
+    }
+    for (i = 0; i < N; ++i) {
+        float fu = (float)FT[i];
+        if (nan_as_inf(fu) <= nan_as_inf(f[i])) {
+            memcpy(X + i * D, T + i * D, sizeof(float) * (size_t)D);
+            f[i] = fu;
+            F64[i] = FT[i];
+        }
+    }
+    free(T);
+    free(FT);
+}

@@ -94,6 +94,28 @@ void oracle_cso_generation(int problem, int64_t N, int64_t D, int64_t B, uint64_
                            uint64_t seed, float phi, const float* lb, const float* ub,
                            float* X, float* V, float* f, double* F64, int threads);
 
+/* DE/rand/1/bin (Storn & Price 1997, the DE of the paper's experiment P:700,
+ * P:748-750), reading R-14 of DESIGN.md. */
+/* Donor indices of target i at generation t: the word stream
+ * philox((c, i, t, 8), seed)[l], c = 0,1,.. l = 0..3, each mapped to [0,N) by
+ * (w * N) >> 32; r1 = first != i, r2 = next not in {i,r1}, r3 = next not in
+ * {i,r1,r2}.  N >= 4. */
+void oracle_de_indices(int64_t N, int64_t i, uint64_t t, uint64_t seed, int64_t out[3]);
+/* Forced crossover dimension: (philox((0, i, t, 9), seed)[0] * D) >> 32. */
+int64_t oracle_de_jrand(int64_t D, int64_t i, uint64_t t, uint64_t seed);
+/* Trial with caller-supplied crossover uniforms U[D]: v = fmaf(F, xb - xc, xa);
+ * u_j = clip(U_j < CR || j == jrand ? v_j : xi_j). */
+void oracle_de_trial_with(int64_t D, const float* xi, const float* xa, const float* xb,
+                          const float* xc, const float* U, int64_t jrand, float F, float CR,
+                          const float* lb, const float* ub, float* u);
+/* One synchronous DE generation at t, in place: every trial is built from the
+ * population of generation t (U_j = uniform24(philox((j/4, i, t, 10))[j%4])),
+ * evaluated (fp64), and replaces its target iff f(u) <= f(x) with NaN ranked
+ * as +inf.  f = f32 of F64. */
+void oracle_de_generation(int problem, int64_t N, int64_t D, float* X, float* f, double* F64,
+                          float F, float CR, uint64_t t, uint64_t seed, const float* lb,
+                          const float* ub, int threads);
+
 #ifdef __cplusplus
 }
 #endif

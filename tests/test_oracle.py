@@ -383,3 +383,100 @@ def test_cso_generation_invariants(N, B):
         assert f.min() <= f0.min()
         assert (X >= np.float32(-5.12)).all() and (X <= np.float32(5.12)).all()
         assert np.array_equal(f, O.evaluate("rastrigin", X).astype(np.float32))
+
+
+# -------------------------------------------------------------------- DE
+def test_de_spec_examples(golden_dir):
+    """S:328-329 (golden/de_examples.txt): mutant = x_a + F (x_b - x_c)."""
+    for line in open(os.path.join(golden_dir, "de_examples.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        v = [float(x) for x in line.split()]
+        F, xa, xb, xc, m = v[0], v[1:3], v[3:5], v[5:7], v[7:9]
+        u = O.de_trial_with(np.zeros(2), xa, xb, xc, np.zeros(2), 0, F, 1.0)
+        assert list(u) == m
+
+
+def test_de_crossover_extremes_and_clip():
+    xi = np.array([1, 2, 3, 4, 5], np.float32)
+    xa = np.array([10, 20, 30, 40, 50], np.float32)
+    z = np.zeros(5, np.float32)
+    U = np.array([0.1, 0.95, 0.5, 0.99, 0.0], np.float32)
+    # CR = 0: only the forced dimension takes the mutant
+    assert list(O.de_trial_with(xi, xa, z, z, U, 3, 0.5, 0.0)) == [1, 2, 3, 40, 5]
+    # CR = 1: the mutant everywhere
+    assert list(O.de_trial_with(xi, xa, z, z, U, 3, 0.5, 1.0)) == [10, 20, 30, 40, 50]
+    # U_j < CR picks the mutant (strict), plus j_rand
+    assert list(O.de_trial_with(xi, xa, z, z, U, 1, 0.5, 0.5)) == [10, 20, 3, 4, 50]
+    # clip to the bounds
+    assert list(O.de_trial_with(xi, xa, z, z, U, 1, 0.5, 1.0, lb=0, ub=25)) == [10, 20, 25, 25, 25]
+    # F multiplies (x_b - x_c), not (x_c - x_b)
+    u = O.de_trial_with(z, z, np.full(5, 3, np.float32), np.full(5, 1, np.float32), U, 0, 0.5, 1.0)
+    assert (u == 1.0).all()
+
+
+def test_de_indices_forced_set_and_distinct():
+    """pool 4, exclude 0 -> a permutation of {1,2,3}; no duplicates."""
+    for t in range(50):
+        for i in range(4):
+            r = O.de_indices(4, i, t, 7)
+            assert sorted(r) == sorted({0, 1, 2, 3} - {i})
+    rng = np.random.default_rng(0)
+    for _ in range(2000):
+        N = int(rng.integers(4, 10 ** 6))
+        i = int(rng.integers(0, N))
+        r = O.de_indices(N, i, int(rng.integers(0, 1000)), 3)
+        assert len(set(r)) == 3 and i not in r and all(0 <= v < N for v in r)
+
+
+def test_de_indices_uniform_and_keyed():
+    N = 20
+    counts = np.zeros(N)
+    for t in range(3000):
+        for v in O.de_indices(N, 5, t, 11):
+            counts[v] += 1
+    assert counts[5] == 0
+    exp = counts.sum() / (N - 1)
+    chi2 = (((counts - exp) ** 2) / exp)[np.arange(N) != 5].sum()
+    assert chi2 < 43.8  # chi^2_18, p = 0.001
+    assert O.de_indices(1000, 1, 0, 1) != O.de_indices(1000, 1, 1, 1)
+    assert O.de_indices(1000, 1, 0, 1) == O.de_indices(1000, 1, 0, 1)
+    js = [O.de_jrand(10, i, 0, 2) for i in range(2000)]
+    assert min(js) == 0 and max(js) == 9
+
+
+def test_de_generation_greedy_ties_and_monotone():
+    """S:325 trial replaces target iff f(trial) <= f(target); S:330 monotone best."""
+    N, D = 30, 6
+    X, f, F64 = O.de_init("sphere", N, D, -5.12, 5.12, 9)
+    best = [f.min()]
+    for t in range(40):
+        X0, f0 = X.copy(), f.copy()
+        O.de_generation("sphere", X, f, F64, t, 9, -5.12, 5.12)
+        changed = (X != X0).any(1)
+        assert (f[changed] <= f0[changed]).all() and (f <= f0).all()
+        assert np.array_equal(f, O.evaluate("sphere", X).astype(np.float32))
+        assert (X >= np.float32(-5.12)).all() and (X <= np.float32(5.12)).all()
+        best.append(f.min())
+    assert (np.diff(best) <= 0).all() and best[-1] < best[0] * 1e-2
+    # ties (S:325 "<="): 1-D Sphere on points +-1 with F = 1, CR = 1 and bounds [-1, 1]:
+    # every trial clip(x_a + x_b - x_c) is +-1, so f(trial) == f(target) == 1 and EVERY
+    # target must be replaced by its trial (a strict "<" would leave X unchanged).
+    Xc = np.array([[1.0], [-1.0], [1.0], [1.0], [-1.0], [-1.0], [1.0], [-1.0]], np.float32)
+    fc = O.evaluate("sphere", Xc).astype(np.float32)
+    Fc = fc.astype(np.float64)
+    X0 = Xc.copy()
+    O.de_generation("sphere", Xc, fc, Fc, 0, 1, -1, 1, F=1.0, CR=1.0)
+    trials = []
+    for i in range(8):
+        a, b, c = O.de_indices(8, i, 0, 1)
+        trials.append(O.de_trial_with(X0[i], X0[a], X0[b], X0[c], [0.5], 0, 1.0, 1.0, -1, 1))
+    trials = np.array(trials, np.float32)
+    assert np.array_equal(Xc, trials) and not np.array_equal(trials, X0)
+
+
+def test_de_convergence_smoke():
+    X, f, F64 = O.de_init("sphere", 50, 10, -5.12, 5.12, 0)
+    for t in range(300):
+        O.de_generation("sphere", X, f, F64, t, 0, -5.12, 5.12)
+    assert f.min() < 1e-8
