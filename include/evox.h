@@ -75,6 +75,7 @@ typedef enum {
 
 typedef struct evox_pso evox_pso; /* opaque handles */
 typedef struct evox_cso evox_cso;
+typedef struct evox_de evox_de;
 
 /* Per-handle execution options (all optional: pass NULL for the defaults). */
 typedef struct {
@@ -251,6 +252,35 @@ evox_status evox_cso_set_timing(evox_cso* s, int enable);
 evox_status evox_cso_kernel_time(evox_cso* s, double* total_ms, int64_t* gens, int64_t* launches,
                                  int reset);
 evox_status evox_cso_destroy(evox_cso* s);
+
+/* ---------------------------------------------------------------- DE */
+/* DE/rand/1/bin (Storn & Price 1997; the DE of the paper's scaling
+ * experiment; reading R-14).  Each
+ * generation builds, for every target i, three distinct donors r1,r2,r3 != i
+ * (rejection sampling on a Philox word stream: O(1) per target at any pop),
+ * the mutant v = fmaf(F, x_r2 - x_r3, x_r1), the binomial crossover with rate
+ * CR and a forced dimension, clips it to [lb,ub], evaluates it and replaces
+ * the target iff f(trial) <= f(target) (NaN ranks as +inf).  F finite,
+ * CR in [0,1] (defaults 0.5, 0.9); pop >= 4, else EVOX_ERR_CONFIG.
+ * Single GPU in this version (world > 1 -> EVOX_ERR_CONFIG: donors would be
+ * gathered across shards).  The first step evaluates X0 (generation 0). */
+evox_status evox_de_workspace_bytes(int64_t pop, int64_t dim, size_t* bytes);
+evox_status evox_de_init(int64_t pop, int64_t dim, const float* lb, const float* ub, float F,
+                         float CR, uint64_t seed, const evox_opts* opts, evox_de** out);
+evox_status evox_de_step(evox_de* s, evox_problem problem, int64_t n_gens);
+/* Synchronising: minimum fitness of the current population, its index, row. */
+evox_status evox_de_best(evox_de* s, float* fit, int64_t* global_index, float* row_host);
+evox_status evox_de_history(evox_de* s, float* best_per_gen, int64_t cap, int64_t* n);
+/* EVOX_FIELD_X (current population, gathered into one buffer first) or
+ * EVOX_FIELD_F.  Synchronising; valid until the next step. */
+evox_status evox_de_view(evox_de* s, int field, void** dev, int64_t* rows, int64_t* ld);
+evox_status evox_de_info(evox_de* s, int64_t* pop, int64_t* dim, int64_t* ld, int64_t* row0,
+                         int64_t* rows, int64_t* t, void** cuda_stream);
+evox_status evox_de_sync(evox_de* s);
+evox_status evox_de_set_timing(evox_de* s, int enable);
+evox_status evox_de_kernel_time(evox_de* s, double* total_ms, int64_t* gens, int64_t* launches,
+                                int reset);
+evox_status evox_de_destroy(evox_de* s);
 
 /* ---------------------------------------------------------------- test hooks */
 /* out[4i..4i+3] = Philox4x32-10(ctr[4i..4i+3], (key0,key1)) computed by the

@@ -1359,6 +1359,263 @@ evox_status evox_cso_destroy(evox_cso* s) {
     return EVOX_OK;
 }
 
+}  // extern "C"
+
+// ============================================================== DE handle
+struct evox_de : Base {
+    float F = 0.5f, CR = 0.9f;
+    float* buf[2] = {nullptr, nullptr};
+    unsigned char* sel[2] = {nullptr, nullptr};
+    float* f[2] = {nullptr, nullptr};
+    int gen_grid[5] = {0, 0, 0, 0, 0};
+    evox::DeArgs args() const {
+        evox::DeArgs a;
+        std::memset(&a, 0, sizeof a);
+        for (int i = 0; i < 2; ++i) {
+            a.buf[i] = buf[i];
+            a.sel[i] = sel[i];
+            a.f[i] = f[i];
+        }
+        a.lb = lb_d; a.ub = ub_d; a.lb0 = lb[0]; a.ub0 = ub[0];
+        a.uniform_bounds = uniform ? 1 : 0;
+        a.rows = rows; a.row0 = row0; a.D = dim; a.ld = ld; a.pop = pop;
+        a.F = F; a.CR = CR;
+        a.k0 = (unsigned)(seed & 0xffffffffu);
+        a.k1 = (unsigned)(seed >> 32);
+        a.rk = evox::Philox::schedule(seed);
+        a.ctl = ctl;
+        return a;
+    }
+};
+
+namespace {
+
+void de_layout(evox_de* s, Carver& c) {
+    const size_t mat = sizeof(float) * (size_t)s->rows * (size_t)s->ld;
+    c.add(&s->buf[0], mat);
+    c.add(&s->buf[1], mat);
+    c.add(&s->sel[0], s->rows);
+    c.add(&s->sel[1], s->rows);
+    c.add(&s->f[0], sizeof(float) * s->rows);
+    c.add(&s->f[1], sizeof(float) * s->rows);
+    c.add(&s->lb_d, sizeof(float) * s->ld);
+    c.add(&s->ub_d, sizeof(float) * s->ld);
+    c.add(&s->ctl, sizeof(Ctl));
+}
+
+evox_status check_de(evox_de* s) {
+    if (!s) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL handle");
+    if (s->poisoned) return fail(EVOX_ERR_POISONED, "handle poisoned by an earlier CUDA error");
+    return EVOX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+evox_status evox_de_workspace_bytes(int64_t pop, int64_t dim, size_t* bytes) {
+    if (!bytes) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL output");
+    if (pop < 4 || dim < 1) return fail(EVOX_ERR_SHAPE, "need pop >= 4 and dim >= 1");
+    evox_de s;
+    s.ld = round4(dim);
+    s.rows = pop;
+    Carver c;
+    de_layout(&s, c);
+    *bytes = c.off;
+    return EVOX_OK;
+}
+
+evox_status evox_de_init(int64_t pop, int64_t dim, const float* lb, const float* ub, float F,
+                         float CR, uint64_t seed, const evox_opts* opts, evox_de** out) {
+    if (!out) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL output handle pointer");
+    *out = nullptr;
+    if (pop < 4) return fail(EVOX_ERR_CONFIG, "DE needs pop >= 4 (got %lld; S:326)", (long long)pop);
+    if (dim < 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "dim must be >= 1");
+    if (pop > 0xFFFFFFFFll) return fail(EVOX_ERR_SHAPE, "pop must be < 2^32");
+    if (!mul_ok(pop, round4(dim), INT64_MAX / 64)) return fail(EVOX_ERR_SHAPE, "pop*dim overflows");
+    if (!std::isfinite(F)) return fail(EVOX_ERR_INVALID_ARGUMENT, "F must be finite");
+    if (!(CR >= 0.0f && CR <= 1.0f)) return fail(EVOX_ERR_INVALID_ARGUMENT, "CR must be in [0,1]");
+    evox_status st = check_bounds(dim, lb, ub);
+    if (st != EVOX_OK) return st;
+    int world, rank;
+    st = check_opts(opts, &world, &rank);
+    if (st != EVOX_OK) return st;
+    if (world > 1) return fail(EVOX_ERR_CONFIG, "DE is single-GPU in this version");
+    evox_de* s = new (std::nothrow) evox_de;
+    if (!s) return fail(EVOX_ERR_OUT_OF_MEMORY, "host allocation failed");
+    s->F = F;
+    s->CR = CR;
+    st = base_setup(s, pop, dim, lb, ub, seed, opts, 1, 0);
+    if (st == EVOX_OK) {
+        Carver c;
+        de_layout(s, c);
+        st = base_alloc(s, c, opts);
+    }
+    if (st == EVOX_OK) st = base_common_init(s);
+    if (st == EVOX_OK) {
+        DevGuard g(s->device);
+        cudaError_t e = evox::launch_de_init(s->args(), s->stream);
+        if (e != cudaSuccess) st = poison(s, EVOX_ERR_CUDA, "de init", e);
+        for (int p = 0; p < 5 && st == EVOX_OK; ++p)
+            s->gen_grid[p] = evox::de_gen_grid(p, s->ld, s->rows, s->device);
+    }
+    if (st != EVOX_OK) {
+        std::string keep = t_err;
+        base_release(s);
+        delete s;
+        t_err = keep;
+        return st;
+    }
+    *out = s;
+    return EVOX_OK;
+}
+
+evox_status evox_de_step(evox_de* s, evox_problem problem, int64_t n_gens) {
+    evox_status st = check_de(s);
+    if (st != EVOX_OK) return st;
+    if (!valid_problem(problem)) return fail(EVOX_ERR_INVALID_ARGUMENT, "unknown problem %d", (int)problem);
+    if (n_gens < 0) return fail(EVOX_ERR_INVALID_ARGUMENT, "n_gens must be >= 0");
+    if (s->problem >= 0 && s->problem != (int)problem)
+        return fail(EVOX_ERR_CONTRACT, "handle is bound to problem %d (got %d)", s->problem, (int)problem);
+    if (n_gens > (int64_t)0xFFFFFFFFll - 2 - s->t)
+        return fail(EVOX_ERR_SHAPE, "generation counter would exceed 2^32");
+    DevGuard g(s->device);
+    st = ensure_hist(s, (s->t < 0 ? 0 : s->t) + n_gens + 1);
+    if (st != EVOX_OK) return st;
+    s->problem = (int)problem;
+    const evox::DeArgs a = s->args();
+    if (s->t < 0) {
+        CU(s, evox::launch_eval((int)problem, s->buf[0], s->rows, s->dim, s->ld, s->f[0], s->stream));
+        CU(s, evox::launch_de_tell0(a, s->stream));
+        s->t = 0;
+    }
+    if (n_gens == 0) return EVOX_OK;
+    const int grid = s->gen_grid[problem];
+    st = run_graphed(s, (int)problem, n_gens, [&]() -> evox_status {
+        CU(s, timed(s, [&] { return evox::launch_de_gen((int)problem, a, grid, s->stream); }));
+        return EVOX_OK;
+    });
+    if (st != EVOX_OK) return st;
+    s->t += n_gens;
+    return EVOX_OK;
+}
+
+evox_status evox_de_sync(evox_de* s) {
+    evox_status st = check_de(s);
+    if (st != EVOX_OK) return st;
+    return sync_check(s);
+}
+
+evox_status evox_de_view(evox_de* s, int field, void** dev, int64_t* rows, int64_t* ld) {
+    evox_status st = check_de(s);
+    if (st != EVOX_OK) return st;
+    if (!dev) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL output");
+    DevGuard g(s->device);
+    const int p = (int)((s->t < 0 ? 0 : s->t) & 1);
+    int64_t r = s->rows, l = s->ld;
+    switch (field) {
+        case EVOX_FIELD_X:
+            CU(s, evox::launch_de_materialize(s->args(), s->stream));
+            *dev = s->buf[0];
+            break;
+        case EVOX_FIELD_F: *dev = s->f[p]; l = 1; break;
+        default: return fail(EVOX_ERR_INVALID_ARGUMENT, "field %d not available for DE", field);
+    }
+    if (rows) *rows = r;
+    if (ld) *ld = l;
+    return sync_check(s);
+}
+
+evox_status evox_de_best(evox_de* s, float* fit, int64_t* global_index, float* row_host) {
+    evox_status st = check_de(s);
+    if (st != EVOX_OK) return st;
+    DevGuard g(s->device);
+    const int p = (int)((s->t < 0 ? 0 : s->t) & 1);
+    CU(s, evox::launch_argmin_rows(s->f[p], s->rows, s->row0, s->scratch_key, s->stream));
+    if (row_host) CU(s, evox::launch_de_materialize(s->args(), s->stream));
+    st = sync_check(s);
+    if (st != EVOX_OK) return st;
+    unsigned long long key = 0;
+    CU(s, cudaMemcpy(&key, s->scratch_key, sizeof key, cudaMemcpyDeviceToHost));
+    float fv = INFINITY;
+    int64_t gi = -1;
+    if (key != ~0ull) {
+        const uint32_t o = (uint32_t)(key >> 32);
+        const uint32_t bits = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+        std::memcpy(&fv, &bits, 4);
+        gi = (int64_t)(uint32_t)(key & 0xffffffffu);
+    }
+    if (fit) *fit = fv;
+    if (global_index) *global_index = gi;
+    if (row_host && gi >= 0)
+        CU(s, cudaMemcpy(row_host, s->buf[0] + gi * s->ld, 4 * s->dim, cudaMemcpyDeviceToHost));
+    return EVOX_OK;
+}
+
+evox_status evox_de_history(evox_de* s, float* best_per_gen, int64_t cap, int64_t* n) {
+    evox_status st = check_de(s);
+    if (st != EVOX_OK) return st;
+    if (cap < 0 || (cap > 0 && !best_per_gen)) return fail(EVOX_ERR_INVALID_ARGUMENT, "bad buffer");
+    st = sync_check(s);
+    if (st != EVOX_OK) return st;
+    const int64_t T = s->t + 1;
+    if (n) *n = T;
+    const int64_t k = T < cap ? T : cap;
+    DevGuard g(s->device);
+    if (k > 0) CU(s, cudaMemcpy(best_per_gen, s->hist, sizeof(float) * k, cudaMemcpyDeviceToHost));
+    return EVOX_OK;
+}
+
+evox_status evox_de_info(evox_de* s, int64_t* pop, int64_t* dim, int64_t* ld, int64_t* row0,
+                         int64_t* rows, int64_t* t, void** cuda_stream) {
+    if (!s) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL handle");
+    if (pop) *pop = s->pop;
+    if (dim) *dim = s->dim;
+    if (ld) *ld = s->ld;
+    if (row0) *row0 = s->row0;
+    if (rows) *rows = s->rows;
+    if (t) *t = s->t;
+    if (cuda_stream) *cuda_stream = s->stream;
+    return s->poisoned ? fail(EVOX_ERR_POISONED, "handle poisoned") : EVOX_OK;
+}
+
+evox_status evox_de_set_timing(evox_de* s, int enable) {
+    evox_status st = check_de(s);
+    if (st != EVOX_OK) return st;
+    s->timing = enable != 0;
+    return EVOX_OK;
+}
+
+evox_status evox_de_kernel_time(evox_de* s, double* total_ms, int64_t* gens, int64_t* launches,
+                                int reset) {
+    evox_status st = check_de(s);
+    if (st != EVOX_OK) return st;
+    st = sync_check(s);
+    if (st != EVOX_OK) return st;
+    DevGuard g(s->device);
+    CU(s, collect_timing(s));
+    if (total_ms) *total_ms = s->kernel_ms;
+    if (gens) *gens = s->kernel_n;
+    if (launches) *launches = s->kernel_launches;
+    if (reset) {
+        s->kernel_ms = 0.0;
+        s->kernel_n = 0;
+        s->kernel_launches = 0;
+    }
+    return EVOX_OK;
+}
+
+evox_status evox_de_destroy(evox_de* s) {
+    if (!s) return EVOX_OK;
+    base_release(s);
+    delete s;
+    return EVOX_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
 evox_status evox_debug_philox(const uint32_t* ctr, uint32_t key0, uint32_t key1, uint32_t* out,
                               int64_t n, void* cuda_stream) {
     if (n < 0) return fail(EVOX_ERR_INVALID_ARGUMENT, "n must be >= 0");

@@ -75,6 +75,24 @@ struct CsoArgs {
     int exchange;  // 1: per-generation keys go to hkeys for one NCCL min-reduction per call
 };
 
+// DE/rand/1/bin (R-14).  The population lives in two buffers; sel[p][i] says
+// which one holds row i at parity p = t & 1.  A trial is written into the
+// other buffer and adopted by flipping sel[p^1][i] (no copy back).
+struct DeArgs {
+    float* buf[2];          // [rows x ld] each
+    unsigned char* sel[2];  // [rows] per parity
+    float* f[2];            // [rows] per parity
+    const float* lb;
+    const float* ub;
+    float lb0, ub0;
+    int uniform_bounds;
+    long long rows, row0, D, ld, pop;
+    float F, CR;
+    unsigned int k0, k1;
+    PhiloxKey rk;
+    Ctl* ctl;
+};
+
 // Launch configuration is a function of dim only (R-11: bitwise identical
 // results for every shard count and population size).
 int wpr_for_dim(long long ld);
@@ -103,6 +121,12 @@ cudaError_t launch_cso_hist_from_keys(const CsoArgs& a, unsigned long long t0, l
                                       cudaStream_t st);
 cudaError_t launch_argmin_rows(const float* f, long long rows, long long row0,
                                unsigned long long* key_out, cudaStream_t st);
+
+cudaError_t launch_de_init(const DeArgs& a, cudaStream_t st);
+cudaError_t launch_de_tell0(const DeArgs& a, cudaStream_t st);
+int de_gen_grid(int problem, long long ld, long long rows, int device);
+cudaError_t launch_de_gen(int problem, const DeArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_de_materialize(const DeArgs& a, cudaStream_t st);
 
 cudaError_t launch_debug_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
                                 long long n, cudaStream_t st);

@@ -104,6 +104,17 @@ SIGNATURES = {
     "evox_cso_destroy": ([_p], _i),
     "evox_cso_set_timing": ([_p, _i], _i),
     "evox_cso_kernel_time": ([_p, ctypes.POINTER(ctypes.c_double), _PI64, _PI64, _i], _i),
+    "evox_de_workspace_bytes": ([_i64, _i64, _PSZ], _i),
+    "evox_de_init": ([_i64, _i64, _p, _p, _f32, _f32, _u64, _p, _PP], _i),
+    "evox_de_step": ([_p, _i, _i64], _i),
+    "evox_de_best": ([_p, _PF32, _PI64, _p], _i),
+    "evox_de_history": ([_p, _p, _i64, _PI64], _i),
+    "evox_de_view": ([_p, _i, _PP, _PI64, _PI64], _i),
+    "evox_de_info": ([_p, _PI64, _PI64, _PI64, _PI64, _PI64, _PI64, _PP], _i),
+    "evox_de_sync": ([_p], _i),
+    "evox_de_set_timing": ([_p, _i], _i),
+    "evox_de_kernel_time": ([_p, ctypes.POINTER(ctypes.c_double), _PI64, _PI64, _i], _i),
+    "evox_de_destroy": ([_p], _i),
     "evox_debug_philox": ([_p, _u32, _u32, _p, _i64, _p], _i),
 }
 
@@ -436,3 +447,30 @@ class CSO(_Handle):
 
     def step(self, problem, n_gens: int = 1):
         _check(lib().evox_cso_step(self._h, problem_id(problem), int(n_gens)))
+
+
+class DE(_Handle):
+    """DE/rand/1/bin (the DE of the paper's experiment; R-14)."""
+    _prefix = "de"
+
+    def __init__(self, pop: int, dim: int, lb=-5.12, ub=5.12, F: float = 0.5, CR: float = 0.9,
+                 seed: int = 0, stream=None, device: Optional[int] = None, workspace=None):
+        self._h = None
+        self.pop, self.dim = int(pop), int(dim)
+        lbv, ubv = _bounds(lb, ub, self.dim)
+        opts, self._keep = _opts(stream, 0, 1, device, None, workspace)
+        h = ctypes.c_void_p()
+        _check(lib().evox_de_init(self.pop, self.dim, lbv.ctypes.data, ubv.ctypes.data, float(F),
+                                  float(CR), int(seed) & 0xFFFFFFFFFFFFFFFF, ctypes.byref(opts),
+                                  ctypes.byref(h)))
+        self._h = h.value
+        self.device = _device_of(device)
+
+    @staticmethod
+    def workspace_bytes(pop, dim) -> int:
+        b = ctypes.c_size_t()
+        _check(lib().evox_de_workspace_bytes(pop, dim, ctypes.byref(b)))
+        return b.value
+
+    def step(self, problem, n_gens: int = 1):
+        _check(lib().evox_de_step(self._h, problem_id(problem), int(n_gens)))

@@ -1,0 +1,132 @@
+"""GPU parity of DE/rand/1/bin (R-14) against the CPU oracle."""
+import numpy as np
+import pytest
+
+import oracle as O
+from parity import assert_fitness, near_tie
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2301_12457_b200 as ev  # noqa: E402
+from paper_2301_12457_b200 import evox as E  # noqa: E402
+from paper_2301_12457_b200 import workloads as WL  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    torch.cuda.set_device(0)
+
+
+def _state(de, D):
+    return de.view("X").cpu().numpy()[:, :D].copy(), de.view("F").cpu().numpy().copy()
+
+
+def _de_parity(problem, N, D, seed, gens, F=0.5, CR=0.9, lb=None, ub=None):
+    lo, hi = WL.BOUNDS[problem]
+    lb = lo if lb is None else lb
+    ub = hi if ub is None else ub
+    de = ev.DE(N, D, lb, ub, F=F, CR=CR, seed=seed)
+    de.step(problem, 0)
+    X, f, F64 = O.de_init(problem, N, D, lb, ub, seed)
+    Xg, fg = _state(de, D)
+    assert np.array_equal(Xg, X)
+    assert_fitness(fg, F64, "t=0 f")
+    f = fg.copy()  # decisions from here on use the GPU's fp32 fitness
+    resync = 0
+    for t in range(gens):
+        X0 = X.copy()
+        de.step(problem, 1)
+        O.de_generation(problem, X, f, F64, t, seed, lb, ub, F=F, CR=CR)
+        Xg, fg = _state(de, D)
+        diff = np.nonzero((Xg != X).any(1))[0]
+        for i in diff:
+            # a flipped accept/reject decision: both candidates must be near-tied
+            r = O.de_indices(N, i, t, seed)
+            U = O.draw(1, D, i, t, 10, seed)[0]
+            u = O.de_trial_with(X0[i], X0[r[0]], X0[r[1]], X0[r[2]], U, O.de_jrand(D, i, t, seed),
+                                F, CR, lb, ub)
+            fu = float(O.evaluate(problem, u[None])[0])
+            fx = float(O.evaluate(problem, X0[i][None])[0])
+            assert near_tie(fu, fx), (t, i, fu, fx)
+        if diff.size:
+            resync += 1
+            X = Xg.copy()
+        assert_fitness(fg, O.evaluate(problem, Xg), f"t={t + 1} f")
+        f = fg.copy()
+        F64 = O.evaluate(problem, X)
+    h = de.history()
+    assert len(h) == gens + 1 and (np.diff(h) <= 0).all()
+    return de, resync
+
+
+@pytest.mark.parametrize("problem,N,D", [("sphere", 50, 10), ("ackley", 64, 37),
+                                         ("rastrigin", 40, 100), ("griewank", 33, 1000),
+                                         ("rosenbrock", 20, 4099), ("ackley", 9, 40001)])
+def test_de_parity(problem, N, D):
+    gens = 25 if D <= 1000 else 4
+    _, resync = _de_parity(problem, N, D, seed=3, gens=gens)
+    assert resync <= 2
+
+
+def test_de_crossover_extremes_and_per_dim_bounds():
+    _de_parity("sphere", 16, 9, seed=1, gens=6, CR=0.0)
+    _de_parity("sphere", 16, 9, seed=1, gens=6, CR=1.0, F=0.8)
+    lb = np.linspace(-5, -1, 13).astype(np.float32)
+    ub = np.linspace(1, 5, 13).astype(np.float32)
+    de, _ = _de_parity("rastrigin", 24, 13, seed=2, gens=6, lb=lb, ub=ub)
+    X, _ = _state(de, 13)
+    assert (X >= lb).all() and (X <= ub).all()
+
+
+def test_de_graphed_equals_stepwise_and_view_neutral():
+    N, D, p = 70, 45, "ackley"
+    a = ev.DE(N, D, -32.768, 32.768, seed=5)
+    a.step(p, 40)
+    b = ev.DE(N, D, -32.768, 32.768, seed=5)
+    b.step(p, 0)
+    for _ in range(40):
+        b.step(p, 1)
+        b.view("X")  # gathers the population into one buffer: must not change the trajectory
+    assert np.array_equal(_state(a, D)[0], _state(b, D)[0])
+    assert np.array_equal(a.history(), b.history())
+    fa, ia, ra = a.best()
+    assert fa == a.view("F").cpu().numpy().min() and np.array_equal(ra, _state(a, D)[0][ia])
+
+
+def test_de_large_population_sampled():
+    """pop 2^20 x 100 (past the paper's 16,384 DE limit): one generation,
+    sampled targets recomputed one by one by the oracle."""
+    N, D, seed, p = 1 << 20, 100, 0, "sphere"
+    de = ev.DE(N, D, -5.12, 5.12, seed=seed)
+    de.step(p, 0)
+    X0 = de.view("X").cpu().numpy()[:, :D].copy()
+    f0 = de.view("F").cpu().numpy().copy()
+    de.step(p, 1)
+    X1 = de.view("X").cpu().numpy()[:, :D]
+    f1 = de.view("F").cpu().numpy()
+    rng = np.random.default_rng(0)
+    for i in rng.integers(0, N, 64):
+        r = O.de_indices(N, int(i), 0, seed)
+        U = O.draw(1, D, int(i), 0, 10, seed)[0]
+        u = O.de_trial_with(X0[i], X0[r[0]], X0[r[1]], X0[r[2]], U, O.de_jrand(D, int(i), 0, seed),
+                            0.5, 0.9, -5.12, 5.12)
+        fu = float(O.evaluate(p, u[None])[0])
+        if near_tie(fu, f0[i]):
+            continue
+        expect = u if fu <= f0[i] else X0[i]
+        assert np.array_equal(X1[i], expect), i
+    assert (f1 <= f0).all()
+
+
+def test_de_config_errors():
+    with pytest.raises(E.ConfigError):
+        ev.DE(3, 4, -1, 1)
+    with pytest.raises(E.InvalidArgument):
+        ev.DE(10, 4, -1, 1, CR=1.5)
+    de = ev.DE(10, 4, -1, 1)
+    de.step("sphere", 1)
+    with pytest.raises(E.ContractError):
+        de.step("ackley", 1)
