@@ -58,10 +58,13 @@ def algorithmic_bytes(cfg, rows):
     PSO: per element X r+w (8), V r+w (8), P read-or-write (4) = 20 B; per row
     imp r+w (2), pf read (4), f write (4) = 10 B (the rare pf write is not counted).
     CSO: per loser element Xl r+w, Vl r+w, Xw read = 20 B, i.e. 10 B per population
-    element; per pair f reads (8) + loser f write (4) = 6 B per row."""
+    element; per pair f reads (8) + loser f write (4) = 6 B per row.
+    DE: per element the target and three donor rows read (16) + the trial written (4)."""
     D = cfg.dim
     if cfg.algo == "pso":
         return 20 * D * rows + 10 * rows
+    if cfg.algo == "de":  # target 4 + three donors 12 + trial write 4; sel 4+1, f 4+4 per row
+        return 20 * D * rows + 13 * rows
     return 10 * D * rows + 6 * rows
 
 
@@ -144,6 +147,13 @@ def cpu_baseline(cfg, target_s=12.0):
         t0 = time.perf_counter()
         O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=2, state=st, threads=cores)
         t_gen = (time.perf_counter() - t0) / 2
+    elif cfg.algo == "de":
+        rows = max(rows, 4)
+        X, f, F64 = O.de_init(cfg.problem, rows, D, lb, ub, 0, threads=cores)
+        t0 = time.perf_counter()
+        for t in range(2):
+            O.de_generation(cfg.problem, X, f, F64, t, 0, lb, ub, threads=cores)
+        t_gen = (time.perf_counter() - t0) / 2
     else:
         B = max(2, rows // 8 if rows % 16 == 0 else rows)
         X, V, f, F64 = O.cso_init(cfg.problem, rows, D, lb, ub, 0, threads=cores)
@@ -175,6 +185,14 @@ def run_reference(args, cfg, rank):
         for i in range(args.warmup + args.steps):
             t0 = time.perf_counter()
             st = O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=1, state=st, threads=cores)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    elif cfg.algo == "de":
+        rows = max(rows, 4)
+        X, f, F64 = O.de_init(cfg.problem, rows, D, lb, ub, 0, threads=cores)
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.de_generation(cfg.problem, X, f, F64, i, 0, lb, ub, threads=cores)
             if i >= args.warmup:
                 times.append(time.perf_counter() - t0)
     else:
@@ -262,9 +280,14 @@ def main():
         torch.cuda.synchronize()
 
     lb, ub = WL.BOUNDS[cfg.problem]
-    Cls = ev.PSO if cfg.algo == "pso" else ev.CSO
-    kw = {} if cfg.algo == "pso" else {"block": cfg.pop // 8 if cfg.pop % 16 == 0 else 0}
-    h = Cls(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world, nccl_id=nid, **kw)
+    if cfg.algo == "de":
+        if world > 1:
+            raise SystemExit("DE is single-GPU in this version")
+        h = ev.DE(cfg.pop, cfg.dim, lb, ub, seed=0)
+    else:
+        Cls = ev.PSO if cfg.algo == "pso" else ev.CSO
+        kw = {} if cfg.algo == "pso" else {"block": cfg.pop // 8 if cfg.pop % 16 == 0 else 0}
+        h = Cls(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world, nccl_id=nid, **kw)
     if peer:  # mailboxes of all ranks mapped into every rank through CUDA IPC
         mine = torch.frombuffer(bytearray(h.mailbox_ipc()), dtype=torch.uint8).to(cdev)
         allh = [torch.zeros(64, dtype=torch.uint8, device=cdev) for _ in range(world)]
