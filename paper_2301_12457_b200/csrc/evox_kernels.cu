@@ -1231,37 +1231,6 @@ struct MoverDe {
 
 __device__ __forceinline__ float nan_inf(float v) { return v != v ? __int_as_float(0x7f800000) : v; }
 
-// A DE target resolved ahead of its processing: donors, the buffers that hold
-// the target and the donors at parity p, the target's fitness.
-// (compact: 32-bit rows, the four buffer flags packed in one word)
-struct DeItem {
-    uint32_t r[3];
-    uint32_t sb;  // bit 0: target's buffer, bits 1..3: donors' buffers
-    float fx;
-    bool ok;
-    __device__ __forceinline__ int si() const { return (int)(sb & 1u); }
-    __device__ __forceinline__ int s(int k) const { return (int)((sb >> (k + 1)) & 1u); }
-};
-__device__ __forceinline__ DeItem de_item(const DeArgs& a, const unsigned char* sel, long long row,
-                                          uint32_t t) {
-    DeItem d;
-    d.ok = row < a.rows;
-    d.r[0] = d.r[1] = d.r[2] = 0;
-    d.sb = 0;
-    d.fx = 0.0f;
-    if (d.ok) {
-        long long r[3];
-        de_indices(a, a.row0 + row, t, r);
-        d.r[0] = (uint32_t)r[0];
-        d.r[1] = (uint32_t)r[1];
-        d.r[2] = (uint32_t)r[2];
-        d.sb = (uint32_t)sel[row] | ((uint32_t)sel[r[0]] << 1) | ((uint32_t)sel[r[1]] << 2) |
-               ((uint32_t)sel[r[2]] << 3);
-        d.fx = a.f[t & 1][row];
-    }
-    return d;
-}
-
 // One DE generation: trial of every target from the population at parity p,
 // evaluation, greedy "<=" replacement by flipping the buffer-select flag.
 template <int P, class G, bool UNI>
@@ -1276,40 +1245,27 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_de_gen(DeArgs a) {
     const unsigned char* sel = a.sel[p];
     NoPrefetch pf;
     unsigned long long best = ~0ull;
-    const long long seg_off = m.qb * 16, seg_bytes = (m.qe - m.qb) * 16;
-    // Targets are resolved two iterations ahead (donor indices + buffer flags:
-    // their loads land during one iteration) and their target/donor rows are
-    // prefetched into L2 during the next: the donors are scattered rows.
-    DeItem cur = de_item(a, sel, m.first, (uint32_t)t);
-    DeItem nxt = de_item(a, sel, m.first + m.stride, (uint32_t)t);
     for (long long it = 0;; ++it) {
         const long long wrow = m.wfirst + it * m.stride;
         if (wrow >= a.rows) break;
         const long long row = m.first + it * m.stride;
         const bool ok = row < a.rows;
-        if (m.sl == 0 && nxt.ok) {
-            const long long nrow = row + m.stride;
-            prefetch_l2(reinterpret_cast<const char*>(a.buf[nxt.si()] + nrow * a.ld) + seg_off,
-                        seg_bytes);
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-                prefetch_l2(reinterpret_cast<const char*>(a.buf[nxt.s(k)] + (long long)nxt.r[k] * a.ld) +
-                                seg_off,
-                            seg_bytes);
-        }
-        const DeItem nn = de_item(a, sel, row + 2 * m.stride, (uint32_t)t);
         MoverDe<UNI> mv(a);
-        const int si = cur.si();
+        int si = 0;
         float fx = 0.0f;
         if (ok) {
+            long long r[3];
+            de_indices(a, a.row0 + row, (uint32_t)t, r);
+            si = sel[row];
+            const int s1 = sel[r[0]], s2 = sel[r[1]], s3 = sel[r[2]];
             mv.Xi = reinterpret_cast<const float4*>(a.buf[si] + row * a.ld);
-            mv.Xa = reinterpret_cast<const float4*>(a.buf[cur.s(0)] + (long long)cur.r[0] * a.ld);
-            mv.Xb = reinterpret_cast<const float4*>(a.buf[cur.s(1)] + (long long)cur.r[1] * a.ld);
-            mv.Xc = reinterpret_cast<const float4*>(a.buf[cur.s(2)] + (long long)cur.r[2] * a.ld);
+            mv.Xa = reinterpret_cast<const float4*>(a.buf[s1] + r[0] * a.ld);
+            mv.Xb = reinterpret_cast<const float4*>(a.buf[s2] + r[1] * a.ld);
+            mv.Xc = reinterpret_cast<const float4*>(a.buf[s3] + r[2] * a.ld);
             mv.Out = reinterpret_cast<float4*>(a.buf[si ^ 1] + row * a.ld);
             const uint4 jw = Philox::run(make_uint4(0u, (uint32_t)(a.row0 + row), (uint32_t)t, 9u), a.rk);
             mv.jrand = (long long)(((unsigned long long)jw.x * (unsigned long long)a.D) >> 32);
-            fx = cur.fx;
+            fx = a.f[p][row];
         } else {
             mv.Xi = mv.Xa = mv.Xb = mv.Xc = nullptr;
             mv.Out = nullptr;
@@ -1330,8 +1286,6 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_de_gen(DeArgs a) {
             const unsigned long long k = make_key(fn, a.row0 + row);
             best = k < best ? k : best;
         }
-        cur = nxt;
-        nxt = nn;
     }
     unsigned long long key;
     if (grid_argmin(a.ctl, best, &key) && threadIdx.x == 0) {
