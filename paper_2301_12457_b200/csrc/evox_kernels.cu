@@ -783,6 +783,205 @@ __global__ void __launch_bounds__(256) k_pso_run_small(PsoArgs a, long long n_ge
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged fused PSO generation (warp-per-row geometry, ld <= 4096).
+// Each warp owns a 2-stage shared-memory ring of {X, V, P} x 128 quads (one
+// lane group).  Lane 0 fills it with cp.async.bulk (1-D TMA, SASS UBLKCP)
+// completing on a per-stage mbarrier: while the warp computes group g from
+// shared memory, group g+1 (possibly the first group of the warp's next row)
+// is in flight -- no registers held by in-flight loads, and the 4 chunks of a
+// group are still computed straight-line (cross-chunk Philox ILP).  Stores go
+// straight from registers (evict-first).  Same arithmetic, reduction tree and
+// decisions as k_pso_gen: bitwise identical (tested).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+constexpr int TMA_GQ = 32 * U;  // quads per group (= G32::GROUP)
+struct TmaStage {
+    float4 x[TMA_GQ], v[TMA_GQ], p[TMA_GQ];
+};
+constexpr size_t TMA_SMEM = sizeof(TmaStage) * 2 * WARPS;  // 96 KB per CTA
+
+template <int P, bool UNI>
+__global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen_tma(PsoArgs a) {
+    using G = Geom<32, 1>;  // the warp-per-row geometry (G32)
+    extern __shared__ __align__(128) unsigned char dyn_smem[];
+    __shared__ __align__(8) uint64_t bars[WARPS][2];
+    __shared__ Fit<P> sh_acc[1];
+    __shared__ float sh_head[1];
+    __shared__ __align__(16) HStore<P> sh_h;
+    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+    const RowMap<G> m(a.ld >> 2);
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    TmaStage* stg = reinterpret_cast<TmaStage*>(dyn_smem) + 2 * wid;
+    uint64_t* bar = bars[wid];
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    pdl_wait();
+    pdl_launch_dependents();
+    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
+    const long long NQ = a.ld >> 2;
+    const long long NG = (NQ + TMA_GQ - 1) / TMA_GQ;  // groups per row
+    const long long n_it = m.wfirst < a.rows ? (a.rows - 1 - m.wfirst) / m.stride + 1 : 0;
+    const long long total = n_it * NG;
+    const float4* X4 = reinterpret_cast<const float4*>(a.X);
+    const float4* V4 = reinterpret_cast<const float4*>(a.V);
+    const float4* P4 = reinterpret_cast<const float4*>(a.P);
+    // pbest-pending flags of the current row and the next two rows of the warp
+    long long row = m.first;
+    bool pend[3];
+    pend[0] = row < a.rows ? a.imp[row] != 0 : true;
+    pend[1] = row + m.stride < a.rows ? a.imp[row + m.stride] != 0 : true;
+    pend[2] = row + 2 * m.stride < a.rows ? a.imp[row + 2 * m.stride] != 0 : true;
+    // lane 0: put group g of the warp's stream in flight (it_cur = current row iteration)
+    auto issue = [&](long long g, long long it_cur) {
+        const long long it = g / NG, gg = g - it * NG;
+        const long long r = m.first + it * m.stride;
+        const long long q0 = gg * TMA_GQ;
+        const long long nq = NQ - q0 < TMA_GQ ? NQ - q0 : TMA_GQ;
+        const int st = (int)(g & 1);
+        const long long d = it - it_cur;
+        const bool pd = d == 0 ? pend[0] : (d == 1 ? pend[1] : pend[2]);
+        const uint32_t bytes = (uint32_t)(nq * 16);
+        fence_proxy_async_smem();  // the warp's generic reads of this stage are done
+        mbar_expect_tx(&bar[st], bytes * (pd ? 2u : 3u));
+        const long long o = r * NQ + q0;
+        tma_load_1d(stg[st].x, X4 + o, bytes, &bar[st]);
+        tma_load_1d(stg[st].v, V4 + o, bytes, &bar[st]);
+        if (!pd) tma_load_1d(stg[st].p, P4 + o, bytes, &bar[st]);
+    };
+    if (lane == 0 && total > 0) issue(0, 0);
+    float pf_old = 0.0f;
+    if (lane == 0 && row < a.rows) pf_old = a.pf[row];
+    Fit<P> acc;
+    float pend_x = 0.0f, head_x = 0.0f;
+    bool hpend = false;
+    unsigned long long best = ~0ull;
+    const float w = a.w, cp = a.cp, cg = a.cg;
+    long long it = 0, gg = 0;
+    for (long long g = 0; g < total; ++g) {
+        if (lane == 0 && g + 1 < total) issue(g + 1, it);  // stage (g+1)&1 was freed by g-1
+        const int st = (int)(g & 1);
+        mbar_wait(&bar[st], (uint32_t)((g >> 1) & 1));
+        const bool ok = row < a.rows;
+        const bool pd = pend[0];
+        const long long q0 = gg * TMA_GQ;
+        const uint32_t row_g = (uint32_t)(a.row0 + row);
+        float4* Xr = reinterpret_cast<float4*>(a.X) + row * NQ;
+        float4* Vr = reinterpret_cast<float4*>(a.V) + row * NQ;
+        float4* Pr = reinterpret_cast<float4*>(a.P) + row * NQ;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long cb = q0 + 32 * u;
+            if (cb >= NQ) break;  // warp-uniform
+            const long long q = cb + lane;
+            const bool valid = ok && q < NQ;
+            float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid) {
+                const int k = 32 * u + lane;
+                const float4 xo = stg[st].x[k];
+                float4 vn = stg[st].v[k];
+                const float4 pb = pd ? xo : stg[st].p[k];
+                if (pd) st_stream(Pr + q, xo);
+                const float4 g4 = __ldg(reinterpret_cast<const float4*>(a.G) + q);
+                const float4 lo = bound4t<UNI>(a.lb, a.lb0, q);
+                const float4 hi = bound4t<UNI>(a.ub, a.ub0, q);
+                const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, (uint32_t)t, 2u), a.rk);
+                const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, (uint32_t)t, 3u), a.rk);
+                xn = xo;
+                pso_elem(xn.x, vn.x, pb.x, g4.x, scaled_u24(b1.x, cp), scaled_u24(b2.x, cg), w, lo.x, hi.x);
+                pso_elem(xn.y, vn.y, pb.y, g4.y, scaled_u24(b1.y, cp), scaled_u24(b2.y, cg), w, lo.y, hi.y);
+                pso_elem(xn.z, vn.z, pb.z, g4.z, scaled_u24(b1.z, cp), scaled_u24(b2.z, cg), w, lo.z, hi.z);
+                pso_elem(xn.w, vn.w, pb.w, g4.w, scaled_u24(b1.w, cp), scaled_u24(b2.w, cg), w, lo.w, hi.w);
+                zero_pad(xn, vn, q, a.D);
+                st_stream(Xr + q, xn);
+                st_stream(Vr + q, vn);
+                fit_quad<P>(acc, xn, 4 * q, a.D, htab);
+            }
+            if constexpr (P == ROSENBROCK) {
+                const float nb = __shfl_down_sync(FULL, xn.x, 1);
+                const float f0 = __shfl_sync(FULL, xn.x, 0);
+                if (cb == 0) head_x = f0;
+                if (lane == 31 && hpend) {
+                    acc.pair(pend_x, f0);
+                    hpend = false;
+                }
+                if (valid && q + 1 < NQ) {
+                    const bool has_next = 4 * q + 4 < a.D;
+                    if (lane < 31) {
+                        if (has_next) acc.pair(xn.w, nb);
+                    } else {
+                        hpend = has_next;
+                        pend_x = xn.w;
+                    }
+                }
+            }
+        }
+        __syncwarp();  // all lanes are done reading stage st (reused by group g+2)
+        if (gg == NG - 1) {  // end of the row
+            const float f = reduce_row<P, G>(acc, a.D, head_x, 0.0f, false, sh_acc, sh_head);
+            if (lane == 0 && ok) {
+                const bool imp = f < pf_old;  // per-row tell (A11)
+                a.f[row] = f;
+                a.imp[row] = imp ? 1 : 0;
+                if (imp) a.pf[row] = f;
+                const unsigned long long k = make_key(f, a.row0 + row);
+                best = k < best ? k : best;
+            }
+            acc = Fit<P>();
+            hpend = false;
+            pend_x = head_x = 0.0f;
+            ++it;
+            gg = 0;
+            row += m.stride;
+            pend[0] = pend[1];
+            pend[1] = pend[2];
+            const long long r2 = row + 2 * m.stride;
+            pend[2] = r2 < a.rows ? a.imp[r2] != 0 : true;
+            if (lane == 0 && row < a.rows) pf_old = a.pf[row];
+        } else {
+            ++gg;
+        }
+    }
+    unsigned long long key;
+    if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
+}
+
 // Unfused ask: move X_t -> X_{t+1} (no evaluation).
 template <class G, bool UNI>
 __global__ void __launch_bounds__(256) k_pso_move(PsoArgs a, unsigned long long t) {
@@ -1474,17 +1673,17 @@ int pso_gen_grid(int problem, long long ld, long long rows, int device) {
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
         g = grid_for((const void*)k_pso_gen<P_, G_, true>, row_units<G_>(rows), device);
     }));
-    return g;
+    return g;  // the TMA variant uses the same grid (2 CTAs/SM: 2 x 96 KB of staging)
 }
 
 // Generation kernels are launched with programmatic stream serialization (PDL):
 // kernel t+1 becomes resident while kernel t retires (EVOX_NO_PDL=1: plain launch).
 template <class K, class A>
-static cudaError_t launch_pdl(K kernel, int grid, const A& a, cudaStream_t st) {
+static cudaError_t launch_pdl(K kernel, int grid, const A& a, cudaStream_t st, size_t smem = 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1494,11 +1693,31 @@ static cudaError_t launch_pdl(K kernel, int grid, const A& a, cudaStream_t st) {
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
+// The TMA-staged kernel serves the warp-per-row geometry (EVOX_NO_TMA=1: the
+// LDG kernel instead, for A/B measurements).
+static bool use_tma(long long ld) { return geom_id(ld) == 1 && U == 4 && !getenv("EVOX_NO_TMA"); }
+
+template <class K>
+static void tma_attr(K kernel) {
+    static bool done = false;  // per instantiation
+    if (!done) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
+        done = true;
+    }
+}
+
 cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st) {
     cudaError_t e = cudaSuccess;
-    EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-        e = launch_pdl(k_pso_gen<P_, G_, U_>, grid, a, st);
-    })));
+    if (use_tma(a.ld)) {
+        EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, {
+            tma_attr(k_pso_gen_tma<P_, U_>);
+            e = launch_pdl(k_pso_gen_tma<P_, U_>, grid, a, st, TMA_SMEM);
+        }));
+    } else {
+        EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+            e = launch_pdl(k_pso_gen<P_, G_, U_>, grid, a, st);
+        })));
+    }
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 

@@ -182,6 +182,24 @@ def test_pso_small_kernel_equals_grid_kernel(problem, N, D, lb, ub, seed, monkey
     assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
 
 
+@pytest.mark.parametrize("problem,N,D", [("ackley", 300, 1000), ("rosenbrock", 77, 1001),
+                                         ("griewank", 64, 4096), ("rastrigin", 130, 600),
+                                         ("sphere", 1000, 300)])
+def test_pso_tma_kernel_equals_ldg_kernel(problem, N, D, monkeypatch):
+    """The TMA-staged generation kernel (warp-per-row geometry) is bitwise identical to the
+    LDG kernel."""
+    lb, ub = WL.BOUNDS[problem]
+    monkeypatch.setenv("EVOX_NO_SMALL", "1")
+    a = ev.PSO(N, D, lb, ub, seed=12)
+    a.step(problem, 9)
+    monkeypatch.setenv("EVOX_NO_TMA", "1")
+    b = ev.PSO(N, D, lb, ub, seed=12)
+    b.step(problem, 9)
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
+        assert np.array_equal(ga[k], gb[k]), k
+
+
 def test_pso_c1_oneshot_matches_oracle():
     """C1 (PSO/Sphere 100x10, 100 generations, seed 0) in one step(100) call."""
     pso = ev.PSO(100, 10, -5.12, 5.12, seed=0)
