@@ -1693,17 +1693,17 @@ static cudaError_t launch_pdl(K kernel, int grid, const A& a, cudaStream_t st, s
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
-// The TMA-staged kernel serves the warp-per-row geometry (EVOX_NO_TMA=1: the
-// LDG kernel instead, for A/B measurements).
-static bool use_tma(long long ld) { return geom_id(ld) == 1 && U == 4 && !getenv("EVOX_NO_TMA"); }
+// The TMA-staged kernel is an opt-in variant (EVOX_TMA=1) of the warp-per-row
+// geometry: measured 4-5 points BELOW the LDG + bulk-L2-prefetch kernel at H
+// and C2, so the LDG kernel is the default.
+static bool use_tma(long long ld) {
+    const char* v = getenv("EVOX_TMA");
+    return geom_id(ld) == 1 && U == 4 && v && *v == '1';
+}
 
 template <class K>
 static void tma_attr(K kernel) {
-    static bool done = false;  // per instantiation
-    if (!done) {
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
-        done = true;
-    }
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
 }
 
 cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st) {

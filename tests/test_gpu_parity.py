@@ -186,13 +186,14 @@ def test_pso_small_kernel_equals_grid_kernel(problem, N, D, lb, ub, seed, monkey
                                          ("griewank", 64, 4096), ("rastrigin", 130, 600),
                                          ("sphere", 1000, 300)])
 def test_pso_tma_kernel_equals_ldg_kernel(problem, N, D, monkeypatch):
-    """The TMA-staged generation kernel (warp-per-row geometry) is bitwise identical to the
-    LDG kernel."""
+    """The TMA-staged generation kernel (opt-in, warp-per-row geometry) is bitwise identical
+    to the default LDG kernel."""
     lb, ub = WL.BOUNDS[problem]
     monkeypatch.setenv("EVOX_NO_SMALL", "1")
+    monkeypatch.setenv("EVOX_TMA", "1")
     a = ev.PSO(N, D, lb, ub, seed=12)
     a.step(problem, 9)
-    monkeypatch.setenv("EVOX_NO_TMA", "1")
+    monkeypatch.setenv("EVOX_TMA", "0")
     b = ev.PSO(N, D, lb, ub, seed=12)
     b.step(problem, 9)
     ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
