@@ -262,8 +262,14 @@ evox_status evox_cso_destroy(evox_cso* s);
  * CR and a forced dimension, clips it to [lb,ub], evaluates it and replaces
  * the target iff f(trial) <= f(target) (NaN ranks as +inf).  F finite,
  * CR in [0,1] (defaults 0.5, 0.9); pop >= 4, else EVOX_ERR_CONFIG.
- * Single GPU in this version (world > 1 -> EVOX_ERR_CONFIG: donors would be
- * gathered across shards).  The first step evaluates X0 (generation 0). */
+ * The first step evaluates X0 (generation 0).  Row-sharded (world > 1, up to
+ * 8): donors are drawn from the WHOLE population, so every rank maps every
+ * other rank's state (evox_de_state -> IPC handle or pointer, then
+ * evox_de_connect before the first step) and reads remote donor rows over
+ * NVLink inside the generation kernel; each generation ends with an in-kernel
+ * barrier + global minimum through per-rank mailboxes (same timeout and
+ * EVOX_ERR_EXCHANGE semantics as evox_pso_connect).  Results are bitwise
+ * identical for every world. */
 evox_status evox_de_workspace_bytes(int64_t pop, int64_t dim, size_t* bytes);
 evox_status evox_de_init(int64_t pop, int64_t dim, const float* lb, const float* ub, float F,
                          float CR, uint64_t seed, const evox_opts* opts, evox_de** out);
@@ -277,6 +283,12 @@ evox_status evox_de_view(evox_de* s, int field, void** dev, int64_t* rows, int64
 evox_status evox_de_info(evox_de* s, int64_t* pop, int64_t* dim, int64_t* ld, int64_t* row0,
                          int64_t* rows, int64_t* t, void** cuda_stream);
 evox_status evox_de_sync(evox_de* s);
+/* The state allocation of this rank: device base pointer and/or its 64-byte
+ * cudaIpcMemHandle (NULL outputs are skipped). */
+evox_status evox_de_state(evox_de* s, void** base, uint8_t ipc[64]);
+/* mode 0: `peers` = world device pointers (evox_de_state bases, same process);
+ * mode 1: world x 64-byte IPC handles (entry `rank` ignored). */
+evox_status evox_de_connect(evox_de* s, int mode, const void* peers);
 evox_status evox_de_set_timing(evox_de* s, int enable);
 evox_status evox_de_kernel_time(evox_de* s, double* total_ms, int64_t* gens, int64_t* launches,
                                 int reset);

@@ -1367,7 +1367,16 @@ struct evox_de : Base {
     float* buf[2] = {nullptr, nullptr};
     unsigned char* sel[2] = {nullptr, nullptr};
     float* f[2] = {nullptr, nullptr};
+    unsigned char* mbox = nullptr;  // 2 x world key slots (carved from the state)
     int gen_grid[5] = {0, 0, 0, 0, 0};
+    // cross-shard donors (evox_de_connect)
+    bool peer = false;
+    unsigned long long peer_timeout_ns = 60ull * 1000 * 1000 * 1000;
+    float* pbuf[evox::kMaxPeers][2] = {};
+    unsigned char* psel[evox::kMaxPeers][2] = {};
+    unsigned char* pmbox[evox::kMaxPeers] = {};
+    long long prow0[evox::kMaxPeers + 1] = {};
+    std::vector<void*> ipc_opened;
     evox::DeArgs args() const {
         evox::DeArgs a;
         std::memset(&a, 0, sizeof a);
@@ -1384,6 +1393,30 @@ struct evox_de : Base {
         a.k1 = (unsigned)(seed >> 32);
         a.rk = evox::Philox::schedule(seed);
         a.ctl = ctl;
+        a.rank = rank;
+        a.world = world;
+        a.peer = peer ? 1 : 0;
+        a.peer_timeout_ns = peer_timeout_ns;
+        if (peer) {
+            for (int r = 0; r < world; ++r) {
+                a.pbuf[r][0] = pbuf[r][0];
+                a.pbuf[r][1] = pbuf[r][1];
+                a.psel[r][0] = psel[r][0];
+                a.psel[r][1] = psel[r][1];
+                a.mbox[r] = pmbox[r];
+                a.prow0[r] = prow0[r];
+            }
+            a.prow0[world] = pop;
+        } else {  // one shard: our own state
+            a.world = 1;
+            a.pbuf[0][0] = buf[0];
+            a.pbuf[0][1] = buf[1];
+            a.psel[0][0] = sel[0];
+            a.psel[0][1] = sel[1];
+            a.mbox[0] = mbox;
+            a.prow0[0] = 0;
+            a.prow0[1] = pop;
+        }
         return a;
     }
 };
@@ -1401,6 +1434,7 @@ void de_layout(evox_de* s, Carver& c) {
     c.add(&s->lb_d, sizeof(float) * s->ld);
     c.add(&s->ub_d, sizeof(float) * s->ld);
     c.add(&s->ctl, sizeof(Ctl));
+    c.add(&s->mbox, (size_t)32 * (s->world > 1 ? s->world : 1));
 }
 
 evox_status check_de(evox_de* s) {
@@ -1440,12 +1474,17 @@ evox_status evox_de_init(int64_t pop, int64_t dim, const float* lb, const float*
     int world, rank;
     st = check_opts(opts, &world, &rank);
     if (st != EVOX_OK) return st;
-    if (world > 1) return fail(EVOX_ERR_CONFIG, "DE is single-GPU in this version");
+    if (world > evox::kMaxPeers)
+        return fail(EVOX_ERR_CONFIG, "DE supports world <= %d", evox::kMaxPeers);
+    if (world > 1 && opts && opts->workspace)
+        return fail(EVOX_ERR_CONFIG, "sharded DE maps the library-allocated state: no workspace");
+    if (opts && opts->nccl_id)
+        return fail(EVOX_ERR_CONFIG, "DE shards connect through evox_de_connect, not NCCL");
     evox_de* s = new (std::nothrow) evox_de;
     if (!s) return fail(EVOX_ERR_OUT_OF_MEMORY, "host allocation failed");
     s->F = F;
     s->CR = CR;
-    st = base_setup(s, pop, dim, lb, ub, seed, opts, 1, 0);
+    st = base_setup(s, pop, dim, lb, ub, seed, opts, world, rank);
     if (st == EVOX_OK) {
         Carver c;
         de_layout(s, c);
@@ -1479,6 +1518,8 @@ evox_status evox_de_step(evox_de* s, evox_problem problem, int64_t n_gens) {
         return fail(EVOX_ERR_CONTRACT, "handle is bound to problem %d (got %d)", s->problem, (int)problem);
     if (n_gens > (int64_t)0xFFFFFFFFll - 2 - s->t)
         return fail(EVOX_ERR_SHAPE, "generation counter would exceed 2^32");
+    if (s->world > 1 && !s->peer)
+        return fail(EVOX_ERR_CONTRACT, "world > 1: call evox_de_connect before stepping");
     DevGuard g(s->device);
     st = ensure_hist(s, (s->t < 0 ? 0 : s->t) + n_gens + 1);
     if (st != EVOX_OK) return st;
@@ -1531,12 +1572,18 @@ evox_status evox_de_best(evox_de* s, float* fit, int64_t* global_index, float* r
     if (st != EVOX_OK) return st;
     DevGuard g(s->device);
     const int p = (int)((s->t < 0 ? 0 : s->t) & 1);
-    CU(s, evox::launch_argmin_rows(s->f[p], s->rows, s->row0, s->scratch_key, s->stream));
-    if (row_host) CU(s, evox::launch_de_materialize(s->args(), s->stream));
+    if (!s->peer) CU(s, evox::launch_argmin_rows(s->f[p], s->rows, s->row0, s->scratch_key, s->stream));
+    if (row_host && !s->peer) CU(s, evox::launch_de_materialize(s->args(), s->stream));
     st = sync_check(s);
     if (st != EVOX_OK) return st;
     unsigned long long key = 0;
-    CU(s, cudaMemcpy(&key, s->scratch_key, sizeof key, cudaMemcpyDeviceToHost));
+    if (s->peer) {  // the global minimum of the last generation, from the barrier
+        Ctl c;
+        CU(s, cudaMemcpy(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost));
+        key = c.min_key;
+    } else {
+        CU(s, cudaMemcpy(&key, s->scratch_key, sizeof key, cudaMemcpyDeviceToHost));
+    }
     float fv = INFINITY;
     int64_t gi = -1;
     if (key != ~0ull) {
@@ -1547,8 +1594,19 @@ evox_status evox_de_best(evox_de* s, float* fit, int64_t* global_index, float* r
     }
     if (fit) *fit = fv;
     if (global_index) *global_index = gi;
-    if (row_host && gi >= 0)
-        CU(s, cudaMemcpy(row_host, s->buf[0] + gi * s->ld, 4 * s->dim, cudaMemcpyDeviceToHost));
+    if (row_host && gi >= 0) {
+        if (!s->peer) {
+            CU(s, cudaMemcpy(row_host, s->buf[0] + gi * s->ld, 4 * s->dim, cudaMemcpyDeviceToHost));
+        } else {  // the owner's current buffer, read through peer memory
+            int w = 0;
+            while (w + 1 < s->world && gi >= s->prow0[w + 1]) ++w;
+            const int64_t lr = gi - s->prow0[w];
+            unsigned char sb = 0;
+            CU(s, cudaMemcpy(&sb, s->psel[w][p] + lr, 1, cudaMemcpyDeviceToHost));
+            CU(s, cudaMemcpy(row_host, s->pbuf[w][sb & 1] + lr * s->ld, 4 * s->dim,
+                             cudaMemcpyDeviceToHost));
+        }
+    }
     return EVOX_OK;
 }
 
@@ -1579,6 +1637,75 @@ evox_status evox_de_info(evox_de* s, int64_t* pop, int64_t* dim, int64_t* ld, in
     return s->poisoned ? fail(EVOX_ERR_POISONED, "handle poisoned") : EVOX_OK;
 }
 
+evox_status evox_de_state(evox_de* s, void** base, uint8_t ipc[64]) {
+    evox_status st = check_de(s);
+    if (st != EVOX_OK) return st;
+    if (!s->own_base) return fail(EVOX_ERR_CONFIG, "the state is a caller workspace: not exportable");
+    if (base) *base = s->base;
+    if (ipc) {
+        DevGuard g(s->device);
+        cudaIpcMemHandle_t h;
+        CU(s, cudaIpcGetMemHandle(&h, s->base));
+        std::memcpy(ipc, &h, 64);
+    }
+    return EVOX_OK;
+}
+
+evox_status evox_de_connect(evox_de* s, int mode, const void* peers) {
+    evox_status st = check_de(s);
+    if (st != EVOX_OK) return st;
+    if (!peers) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL peers");
+    if (mode != 0 && mode != 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
+    if (s->t >= 0) return fail(EVOX_ERR_CONTRACT, "connect before the first step");
+    DevGuard g(s->device);
+    for (int r = 0; r < s->world; ++r) {
+        unsigned char* base = nullptr;
+        if (r == s->rank) {
+            base = static_cast<unsigned char*>(s->base);
+        } else if (mode == 0) {
+            base = static_cast<unsigned char*>(static_cast<void* const*>(peers)[r]);
+            if (!base) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL state pointer for rank %d", r);
+            cudaPointerAttributes at;
+            CU(s, cudaPointerGetAttributes(&at, base));
+            if (at.device != s->device) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else if (e != cudaSuccess) return poison(s, EVOX_ERR_CUDA, "cudaDeviceEnablePeerAccess", e);
+            }
+        } else {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const uint8_t*>(peers) + 64 * r, 64);
+            void* p = nullptr;
+            CU(s, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            s->ipc_opened.push_back(p);
+            base = static_cast<unsigned char*>(p);
+        }
+        // rank r's layout: the same carving with its own shard size
+        evox_de probe;
+        probe.world = s->world;
+        probe.ld = s->ld;
+        shard(s->pop, s->world, r, &probe.row0, &probe.rows);
+        Carver c;
+        de_layout(&probe, c);
+        c.assign(base);
+        s->pbuf[r][0] = probe.buf[0];
+        s->pbuf[r][1] = probe.buf[1];
+        s->psel[r][0] = probe.sel[0];
+        s->psel[r][1] = probe.sel[1];
+        s->pmbox[r] = probe.mbox;
+        s->prow0[r] = probe.row0;
+        probe.lb_d = nullptr;  // nothing owned
+    }
+    st = ensure_hist(s, 1 << 16);  // a step must never synchronise (single-process groups)
+    if (st != EVOX_OK) return st;
+    if (const char* ms = std::getenv("EVOX_PEER_TIMEOUT_MS"))
+        s->peer_timeout_ns = (unsigned long long)std::strtoull(ms, nullptr, 10) * 1000000ull;
+    s->peer = true;
+    for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
+    s->graphs.clear();
+    return EVOX_OK;
+}
+
 evox_status evox_de_set_timing(evox_de* s, int enable) {
     evox_status st = check_de(s);
     if (st != EVOX_OK) return st;
@@ -1607,6 +1734,12 @@ evox_status evox_de_kernel_time(evox_de* s, double* total_ms, int64_t* gens, int
 
 evox_status evox_de_destroy(evox_de* s) {
     if (!s) return EVOX_OK;
+    {
+        DevGuard g(s->device);
+        if (s->stream) cudaStreamSynchronize(s->stream);
+        for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
+        cudaGetLastError();
+    }
     base_release(s);
     delete s;
     return EVOX_OK;

@@ -25,6 +25,7 @@ struct Ctl {
     float* hist;                 // hist[t] = min f of generation t
     unsigned long long* hkeys;   // CSO, world > 1: per-generation local min keys
     unsigned long long hist_cap;
+    unsigned long long min_key;  // DE with peers: global min key of the current population
 };
 
 // One rank's PSO state, as seen by kernels.
@@ -91,6 +92,16 @@ struct DeArgs {
     unsigned int k0, k1;
     PhiloxKey rk;
     Ctl* ctl;
+    // row sharding with cross-shard donors (evox_de_connect): every rank's
+    // buffers and flags (own included; world == 1: just our own), the row
+    // offsets of the shards, and the key-only mailboxes of the per-generation
+    // barrier + global minimum
+    int rank, world, peer;
+    float* pbuf[kMaxPeers][2];
+    unsigned char* psel[kMaxPeers][2];
+    long long prow0[kMaxPeers + 1];
+    unsigned char* mbox[kMaxPeers];
+    unsigned long long peer_timeout_ns;
 };
 
 // Launch configuration is a function of dim only (R-11: bitwise identical

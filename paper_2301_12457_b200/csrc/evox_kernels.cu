@@ -405,13 +405,16 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long k)
 // Every thread calls it after its last row; returns true in the (whole) last
 // CTA to finish, with the generation's min key in *out_key.
 __device__ __forceinline__ bool grid_argmin(Ctl* ctl, unsigned long long my_key,
-                                            unsigned long long* out_key) {
+                                            unsigned long long* out_key, bool sys = false) {
     __shared__ unsigned long long sh_k[32];
     __shared__ int sh_last;
     const int lane = lane_id(), wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
     my_key = warp_min_u64(my_key);
     if (lane == 0) sh_k[wid] = my_key;
-    __threadfence();  // this thread's population stores visible device-wide
+    // this thread's population stores visible device-wide (system-wide when peers
+    // on other GPUs read this shard in the next generation)
+    if (sys) __threadfence_system();
+    else __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long k = sh_k[0];
@@ -1430,6 +1433,64 @@ struct MoverDe {
 
 __device__ __forceinline__ float nan_inf(float v) { return v != v ? __int_as_float(0x7f800000) : v; }
 
+// Owner rank of a global row (linear scan over <= kMaxPeers shard offsets).
+__device__ __forceinline__ int de_owner(const DeArgs& a, long long r) {
+    int w = 0;
+    while (w + 1 < a.world && r >= a.prow0[w + 1]) ++w;
+    return w;
+}
+// Row r of the population at parity p, wherever it lives (peer memory over NVLink).
+__device__ __forceinline__ const float4* de_row(const DeArgs& a, long long r, int p) {
+    const int w = de_owner(a, r);
+    const long long lr = r - a.prow0[w];
+    const int s = a.psel[w][p][lr];
+    return reinterpret_cast<const float4*>(a.pbuf[w][s] + lr * a.ld);
+}
+
+// End-of-generation barrier of the sharded DE: publish this rank's min key in
+// every rank's mailbox (slot[par][rank] = {flag, key}), wait for all, return the
+// global min.  No rank starts generation t+1 (which may overwrite rows peers
+// read as donors in generation t) before every rank finished generation t.
+__device__ unsigned long long de_peer_min(const DeArgs& a, unsigned long long key,
+                                          unsigned long long t_new) {
+    const int par = (int)(t_new & 1);
+    const unsigned long long flag = t_new + 1;
+    const long long my = ((long long)par * a.world + a.rank) * 16;
+    for (int w = 0; w < a.world; ++w)
+        *reinterpret_cast<unsigned long long*>(a.mbox[w] + my + 8) = key;
+    __threadfence_system();
+    for (int w = 0; w < a.world; ++w)
+        st_release_sys(reinterpret_cast<unsigned long long*>(a.mbox[w] + my), flag);
+    unsigned long long kmin = ~0ull;
+    const unsigned long long t0 = globaltimer_ns();
+    for (int w = 0; w < a.world; ++w) {
+        const unsigned char* slot = a.mbox[a.rank] + ((long long)par * a.world + w) * 16;
+        while (ld_acquire_sys(reinterpret_cast<const unsigned long long*>(slot)) != flag) {
+            if (globaltimer_ns() - t0 > a.peer_timeout_ns) {
+                a.ctl->err = 1;
+                break;
+            }
+            __nanosleep(256);
+        }
+        const unsigned long long kw = __ldcg(reinterpret_cast<const unsigned long long*>(slot + 8));
+        kmin = kw < kmin ? kw : kmin;
+    }
+    return kmin;
+}
+
+__device__ __forceinline__ void de_finalize(const DeArgs& a, unsigned long long key,
+                                            unsigned long long t_new) {
+    if (threadIdx.x == 0) {
+        Ctl* ctl = a.ctl;
+        if (a.peer) key = de_peer_min(a, key, t_new);
+        ctl->hist[t_new] = key != ~0ull ? unord_f32((uint32_t)(key >> 32)) : __int_as_float(0x7f800000);
+        ctl->min_key = key;
+        ctl->gen_key = ~0ull;
+        ctl->ticket = 0u;
+        ctl->t = t_new;
+    }
+}
+
 // One DE generation: trial of every target from the population at parity p,
 // evaluation, greedy "<=" replacement by flipping the buffer-select flag.
 template <int P, class G, bool UNI>
@@ -1454,13 +1515,12 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_de_gen(DeArgs a) {
         float fx = 0.0f;
         if (ok) {
             long long r[3];
-            de_indices(a, a.row0 + row, (uint32_t)t, r);
+            de_indices(a, a.row0 + row, (uint32_t)t, r);  // GLOBAL donor rows
             si = sel[row];
-            const int s1 = sel[r[0]], s2 = sel[r[1]], s3 = sel[r[2]];
             mv.Xi = reinterpret_cast<const float4*>(a.buf[si] + row * a.ld);
-            mv.Xa = reinterpret_cast<const float4*>(a.buf[s1] + r[0] * a.ld);
-            mv.Xb = reinterpret_cast<const float4*>(a.buf[s2] + r[1] * a.ld);
-            mv.Xc = reinterpret_cast<const float4*>(a.buf[s3] + r[2] * a.ld);
+            mv.Xa = de_row(a, r[0], p);
+            mv.Xb = de_row(a, r[1], p);
+            mv.Xc = de_row(a, r[2], p);
             mv.Out = reinterpret_cast<float4*>(a.buf[si ^ 1] + row * a.ld);
             const uint4 jw = Philox::run(make_uint4(0u, (uint32_t)(a.row0 + row), (uint32_t)t, 9u), a.rk);
             mv.jrand = (long long)(((unsigned long long)jw.x * (unsigned long long)a.D) >> 32);
@@ -1487,13 +1547,7 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_de_gen(DeArgs a) {
         }
     }
     unsigned long long key;
-    if (grid_argmin(a.ctl, best, &key) && threadIdx.x == 0) {
-        Ctl* ctl = a.ctl;
-        ctl->hist[t + 1] = key != ~0ull ? unord_f32((uint32_t)(key >> 32)) : __int_as_float(0x7f800000);
-        ctl->gen_key = ~0ull;
-        ctl->ticket = 0u;
-        ctl->t = t + 1;
-    }
+    if (grid_argmin(a.ctl, best, &key, a.peer != 0)) de_finalize(a, key, t + 1);
 }
 
 __global__ void k_de_init(DeArgs a) {
@@ -1515,13 +1569,7 @@ __global__ void __launch_bounds__(256) k_de_tell0(DeArgs a) {
         best = k < best ? k : best;
     }
     unsigned long long key;
-    if (grid_argmin(a.ctl, best, &key) && threadIdx.x == 0) {
-        Ctl* ctl = a.ctl;
-        ctl->hist[0] = key != ~0ull ? unord_f32((uint32_t)(key >> 32)) : __int_as_float(0x7f800000);
-        ctl->gen_key = ~0ull;
-        ctl->ticket = 0u;
-        ctl->t = 0;
-    }
+    if (grid_argmin(a.ctl, best, &key, a.peer != 0)) de_finalize(a, key, 0);
 }
 
 // Gather the current population into buf[0] (rows held by buf[1] are copied and

@@ -113,6 +113,8 @@ SIGNATURES = {
     "evox_de_info": ([_p, _PI64, _PI64, _PI64, _PI64, _PI64, _PI64, _PP], _i),
     "evox_de_sync": ([_p], _i),
     "evox_de_set_timing": ([_p, _i], _i),
+    "evox_de_state": ([_p, _PP, _p], _i),
+    "evox_de_connect": ([_p, _i, _p], _i),
     "evox_de_kernel_time": ([_p, ctypes.POINTER(ctypes.c_double), _PI64, _PI64, _i], _i),
     "evox_de_destroy": ([_p], _i),
     "evox_debug_philox": ([_p, _u32, _u32, _p, _i64, _p], _i),
@@ -454,11 +456,12 @@ class DE(_Handle):
     _prefix = "de"
 
     def __init__(self, pop: int, dim: int, lb=-5.12, ub=5.12, F: float = 0.5, CR: float = 0.9,
-                 seed: int = 0, stream=None, device: Optional[int] = None, workspace=None):
+                 seed: int = 0, stream=None, rank: int = 0, world: int = 1,
+                 device: Optional[int] = None, workspace=None):
         self._h = None
         self.pop, self.dim = int(pop), int(dim)
         lbv, ubv = _bounds(lb, ub, self.dim)
-        opts, self._keep = _opts(stream, 0, 1, device, None, workspace)
+        opts, self._keep = _opts(stream, rank, world, device, None, workspace)
         h = ctypes.c_void_p()
         _check(lib().evox_de_init(self.pop, self.dim, lbv.ctypes.data, ubv.ctypes.data, float(F),
                                   float(CR), int(seed) & 0xFFFFFFFFFFFFFFFF, ctypes.byref(opts),
@@ -474,3 +477,21 @@ class DE(_Handle):
 
     def step(self, problem, n_gens: int = 1):
         _check(lib().evox_de_step(self._h, problem_id(problem), int(n_gens)))
+
+    def state_base(self) -> int:
+        p = ctypes.c_void_p()
+        _check(lib().evox_de_state(self._h, ctypes.byref(p), None))
+        return p.value
+
+    def state_ipc(self) -> bytes:
+        buf = (ctypes.c_uint8 * 64)()
+        _check(lib().evox_de_state(self._h, None, buf))
+        return bytes(buf)
+
+    def connect_local(self, bases):
+        arr = (ctypes.c_void_p * len(bases))(*[int(b) for b in bases])
+        _check(lib().evox_de_connect(self._h, 0, arr))
+
+    def connect_ipc(self, handles):
+        buf = ctypes.create_string_buffer(b"".join(bytes(h) for h in handles))
+        _check(lib().evox_de_connect(self._h, 1, buf))

@@ -130,3 +130,47 @@ def test_de_config_errors():
     de.step("sphere", 1)
     with pytest.raises(E.ContractError):
         de.step("ackley", 1)
+
+
+# ------------------------------------------------------- sharded DE (peer memory)
+def _de_group(W, N, D, lb, ub, seed):
+    hs = [ev.DE(N, D, lb, ub, seed=seed, rank=r, world=W, stream=torch.cuda.Stream())
+          for r in range(W)]
+    bases = [h.state_base() for h in hs]
+    for h in hs:
+        h.connect_local(bases)
+    return hs
+
+
+@pytest.mark.parametrize("W,N,D,problem", [(2, 64, 37, "ackley"), (3, 50, 100, "sphere"),
+                                           (4, 97, 1000, "rastrigin"), (8, 203, 20, "griewank"),
+                                           (2, 9, 4099, "rosenbrock")])
+def test_de_sharded_equals_single(W, N, D, problem):
+    """Donors drawn from the whole population, read across shards through peer memory:
+    the sharded trajectory is bitwise the single-shard one."""
+    lb, ub = WL.BOUNDS[problem]
+    ref = ev.DE(N, D, lb, ub, seed=6)
+    ref.step(problem, 30)
+    hs = _de_group(W, N, D, lb, ub, 6)
+    for h in hs:
+        h.step(problem, 0)
+    for _ in range(3):
+        for h in hs:
+            h.step(problem, 10)
+    for h in hs:
+        h.sync()
+    X = np.concatenate([h.view("X").cpu().numpy()[:, :D] for h in hs])
+    F = np.concatenate([h.view("F").cpu().numpy() for h in hs])
+    assert np.array_equal(X, ref.view("X").cpu().numpy()[:, :D])
+    assert np.array_equal(F, ref.view("F").cpu().numpy())
+    rb = ref.best()
+    for h in hs:
+        assert np.array_equal(h.history(), ref.history())
+        b = h.best()
+        assert b[0] == rb[0] and b[1] == rb[1] and np.array_equal(b[2], rb[2])
+
+
+def test_de_sharded_requires_connect():
+    h = ev.DE(16, 4, -1, 1, rank=0, world=2)
+    with pytest.raises(E.ContractError):
+        h.step("sphere", 1)
