@@ -267,7 +267,7 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nid = None
     peer = world > 1 and cfg.algo == "pso" and args.exchange == "peer"
-    if world > 1 and not peer:
+    if world > 1 and not peer and cfg.algo != "de":
         buf = torch.zeros(128, dtype=torch.uint8, device=cdev)
         if rank == 0:
             buf.copy_(torch.frombuffer(bytearray(ev.nccl_unique_id()), dtype=torch.uint8))
@@ -280,10 +280,14 @@ def main():
         torch.cuda.synchronize()
 
     lb, ub = WL.BOUNDS[cfg.problem]
-    if cfg.algo == "de":
+    if cfg.algo == "de":  # shards read donors across GPUs: map every rank's state (IPC)
+        h = ev.DE(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world)
         if world > 1:
-            raise SystemExit("DE is single-GPU in this version")
-        h = ev.DE(cfg.pop, cfg.dim, lb, ub, seed=0)
+            mine = torch.frombuffer(bytearray(h.state_ipc()), dtype=torch.uint8).to(cdev)
+            allh = [torch.zeros(64, dtype=torch.uint8, device=cdev) for _ in range(world)]
+            dist.all_gather(allh, mine)
+            h.connect_ipc([bytes(x.cpu().numpy().tobytes()) for x in allh])
+            barrier()
     else:
         Cls = ev.PSO if cfg.algo == "pso" else ev.CSO
         kw = {} if cfg.algo == "pso" else {"block": cfg.pop // 8 if cfg.pop % 16 == 0 else 0}
