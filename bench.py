@@ -363,7 +363,7 @@ def main():
             "config": {"workload": cfg.note, "algo": cfg.algo, "problem": cfg.problem,
                        "pop": cfg.pop, "dim": cfg.dim, "seed": 0,
                        "parallelism": f"row-sharded x{world}" + (
-                           f", exchange={'peer-memory (in-kernel)' if peer else 'nccl'}"
+                           f", exchange={'peer-memory (in-kernel)' if peer else ('peer-memory donors' if cfg.algo == 'de' else 'nccl')}"
                            if world > 1 else ""),
                        "l2": "state (X,V,P) > L2: inputs larger than L2, no flush needed"
                        if 12 * cfg.pop * cfg.dim > 2 * 126e6 else "state comparable to L2"},

@@ -227,8 +227,13 @@ evox_status evox_pso_destroy(evox_pso* s);
 
 /* ---------------------------------------------------------------- CSO */
 /* Competitive swarm optimizer (Table II; R-8).  pop >= 2; block = the
- * pairing block size B (0 = default pop/8 rounded to a valid size; B >= 2);
- * with world > 1 every shard must hold whole blocks, else EVOX_ERR_CONFIG.
+ * pairing block size B (0 = default pop/8 rounded to a valid size; B >= 2,
+ * B = pop: global pairing).  world > 1: when every shard holds whole blocks
+ * the shards are independent (NCCL only reduces the per-generation minima);
+ * otherwise pairs straddle shards and the ranks must be connected
+ * (evox_cso_state / evox_cso_connect, as for DE): each rank updates the losers
+ * it owns, reading partner fitness and winner rows through peer memory, with
+ * an in-kernel barrier + global minimum per generation.
  * phi: social factor of the mean-position term (0 by default; phi != 0 is
  * supported only for world == 1 in this version -> EVOX_ERR_CONFIG). */
 evox_status evox_cso_workspace_bytes(int64_t pop, int64_t dim, int world, int rank, size_t* bytes);
@@ -248,6 +253,8 @@ evox_status evox_cso_info(evox_cso* s, int64_t* pop, int64_t* dim, int64_t* ld, 
 evox_status evox_cso_load(evox_cso* s, const void* host_blob, size_t size);
 evox_status evox_cso_save(evox_cso* s, void* host_blob, size_t cap, size_t* used);
 evox_status evox_cso_sync(evox_cso* s);
+evox_status evox_cso_state(evox_cso* s, void** base, uint8_t ipc[64]);
+evox_status evox_cso_connect(evox_cso* s, int mode, const void* peers);
 evox_status evox_cso_set_timing(evox_cso* s, int enable);
 evox_status evox_cso_kernel_time(evox_cso* s, double* total_ms, int64_t* gens, int64_t* launches,
                                  int reset);

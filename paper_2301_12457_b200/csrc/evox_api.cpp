@@ -1001,6 +1001,16 @@ evox_status evox_pso_destroy(evox_pso* s) {
 struct evox_cso : Base {
     float phi = 0.0f;
     int64_t B = 0;
+    bool aligned = true;  // every shard holds whole pairing blocks
+    // global pairing across shards (evox_cso_connect)
+    bool peer = false;
+    unsigned long long peer_timeout_ns = 60ull * 1000 * 1000 * 1000;
+    float* pX[evox::kMaxPeers] = {};
+    float* pf[evox::kMaxPeers] = {};
+    unsigned char* pmbox[evox::kMaxPeers] = {};
+    long long prow0[evox::kMaxPeers + 1] = {};
+    std::vector<void*> ipc_opened;
+    unsigned char* mbox = nullptr;
     float *X = nullptr, *V = nullptr, *f = nullptr, *xbar = nullptr;
     double* colpart = nullptr;
     unsigned long long* keybuf = nullptr;
@@ -1019,7 +1029,26 @@ struct evox_cso : Base {
         a.ctl = ctl;
         a.rank = rank;
         a.world = world;
-        a.exchange = comm != nullptr;
+        a.exchange = comm != nullptr && !peer;
+        a.peer = peer ? 1 : 0;
+        a.peer_timeout_ns = peer_timeout_ns;
+        if (peer) {
+            a.nsh = world;
+            for (int r = 0; r < world; ++r) {
+                a.pX[r] = pX[r];
+                a.pf[r] = pf[r];
+                a.mbox[r] = pmbox[r];
+                a.prow0[r] = prow0[r];
+            }
+            a.prow0[world] = pop;
+        } else {  // one table entry: our own shard
+            a.nsh = 1;
+            a.pX[0] = X;
+            a.pf[0] = f;
+            a.mbox[0] = mbox;
+            a.prow0[0] = row0;
+            a.prow0[1] = row0 + rows;
+        }
         return a;
     }
 };
@@ -1035,6 +1064,7 @@ void cso_layout(evox_cso* s, Carver& c) {
     c.add(&s->ub_d, sizeof(float) * s->ld);
     c.add(&s->ctl, sizeof(Ctl));
     c.add(&s->xbar, sizeof(float) * s->ld);
+    c.add(&s->mbox, (size_t)32 * (s->world > 1 ? s->world : 1));
     if (s->phi != 0.0f) c.add(&s->colpart, sizeof(double) * s->ld * ((s->rows + 1023) / 1024));
 }
 
@@ -1086,12 +1116,14 @@ evox_status evox_cso_init(int64_t pop, int64_t dim, const float* lb, const float
     st = check_opts(opts, &world, &rank);
     if (st != EVOX_OK) return st;
     const int64_t B = block == 0 ? default_block(pop) : (block > pop ? pop : block);
+    bool aligned = true;
     if (world > 1) {
-        if (pop % world != 0 || (pop / world) % B != 0)
+        aligned = pop % world == 0 && (pop / world) % B == 0;
+        if (!aligned && (world > evox::kMaxPeers || (opts && opts->workspace)))
             return fail(EVOX_ERR_CONFIG,
-                        "CSO with world %d needs every shard to hold whole pairing blocks "
-                        "(pop %% world == 0 and (pop/world) %% B == 0; pop=%lld, B=%lld)",
-                        world, (long long)pop, (long long)B);
+                        "CSO with world %d and blocks straddling shards (pop=%lld, B=%lld) needs "
+                        "global pairing through evox_cso_connect (world <= %d, no workspace)",
+                        world, (long long)pop, (long long)B, evox::kMaxPeers);
         if (phi != 0.0f)
             return fail(EVOX_ERR_CONFIG, "CSO phi != 0 is supported for world == 1 only");
     }
@@ -1099,6 +1131,7 @@ evox_status evox_cso_init(int64_t pop, int64_t dim, const float* lb, const float
     if (!s) return fail(EVOX_ERR_OUT_OF_MEMORY, "host allocation failed");
     s->phi = phi;
     s->B = B;
+    s->aligned = aligned;
     st = base_setup(s, pop, dim, lb, ub, seed, opts, world, rank);
     if (st == EVOX_OK) {
         Carver c;
@@ -1135,6 +1168,10 @@ evox_status evox_cso_step(evox_cso* s, evox_problem problem, int64_t n_gens) {
         return fail(EVOX_ERR_CONTRACT, "handle is bound to problem %d (got %d)", s->problem, (int)problem);
     if (n_gens > (int64_t)0xFFFFFFFFll - 2 - s->t)
         return fail(EVOX_ERR_SHAPE, "generation counter would exceed 2^32");
+    if (s->world > 1 && !s->peer && (!s->comm || !s->aligned))
+        return fail(EVOX_ERR_CONTRACT,
+                    s->aligned ? "world > 1: pass opts.nccl_id at init or call evox_cso_connect"
+                               : "pairing blocks straddle shards: call evox_cso_connect first");
     DevGuard g(s->device);
     const int64_t t0 = s->t < 0 ? 0 : s->t;
     st = ensure_hist(s, t0 + n_gens + 1);
@@ -1159,7 +1196,7 @@ evox_status evox_cso_step(evox_cso* s, evox_problem problem, int64_t n_gens) {
         if (st != EVOX_OK) return st;
         s->t += n_gens;
     }
-    if (s->comm) {  // one min-reduction of this call's per-generation keys
+    if (s->comm && !s->peer) {  // one min-reduction of this call's per-generation keys
         const int64_t n = s->t - first + 1;
         if (n > 0) {
             const evox::NcclApi* api = evox::nccl_api(nullptr);
@@ -1181,13 +1218,22 @@ evox_status evox_cso_best(evox_cso* s, float* fit, int64_t* global_index, float*
     evox_status st = check_cso(s);
     if (st != EVOX_OK) return st;
     DevGuard g(s->device);
-    CU(s, evox::launch_argmin_rows(s->f, s->rows, s->row0, s->keybuf, s->stream));
-    const evox::NcclApi* api = s->comm ? evox::nccl_api(nullptr) : nullptr;
-    if (api) NC(s, api->AllReduce(s->keybuf, s->keybuf, 1, ncclUint64, ncclMin, s->comm, s->stream));
+    const evox::NcclApi* api = (s->comm && !s->peer) ? evox::nccl_api(nullptr) : nullptr;
+    if (!s->peer) {
+        CU(s, evox::launch_argmin_rows(s->f, s->rows, s->row0, s->keybuf, s->stream));
+        if (api)
+            NC(s, api->AllReduce(s->keybuf, s->keybuf, 1, ncclUint64, ncclMin, s->comm, s->stream));
+    }
     st = sync_check(s);
     if (st != EVOX_OK) return st;
     unsigned long long key = 0;
-    CU(s, cudaMemcpy(&key, s->keybuf, sizeof key, cudaMemcpyDeviceToHost));
+    if (s->peer) {  // global minimum of the last generation, from the in-kernel barrier
+        Ctl c;
+        CU(s, cudaMemcpy(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost));
+        key = c.min_key;
+    } else {
+        CU(s, cudaMemcpy(&key, s->keybuf, sizeof key, cudaMemcpyDeviceToHost));
+    }
     float fv = INFINITY;
     int64_t gi = -1;
     if (key != ~0ull) {
@@ -1198,7 +1244,12 @@ evox_status evox_cso_best(evox_cso* s, float* fit, int64_t* global_index, float*
     }
     if (fit) *fit = fv;
     if (global_index) *global_index = gi;
-    if (row_host && gi >= 0) {
+    if (row_host && gi >= 0 && s->peer) {
+        int w = 0;
+        while (w + 1 < s->world && gi >= s->prow0[w + 1]) ++w;
+        CU(s, cudaMemcpy(row_host, s->pX[w] + (gi - s->prow0[w]) * s->ld, 4 * s->dim,
+                         cudaMemcpyDeviceToHost));
+    } else if (row_host && gi >= 0) {
         const bool mine = gi >= s->row0 && gi < s->row0 + s->rows;
         if (mine)
             CU(s, cudaMemcpyAsync(s->scratch_row, s->X + (gi - s->row0) * s->ld, 4 * s->ld,
@@ -1324,6 +1375,74 @@ evox_status evox_cso_load(evox_cso* s, const void* host_blob, size_t size) {
     return EVOX_OK;
 }
 
+evox_status evox_cso_state(evox_cso* s, void** base, uint8_t ipc[64]) {
+    evox_status st = check_cso(s);
+    if (st != EVOX_OK) return st;
+    if (!s->own_base) return fail(EVOX_ERR_CONFIG, "the state is a caller workspace: not exportable");
+    if (base) *base = s->base;
+    if (ipc) {
+        DevGuard g(s->device);
+        cudaIpcMemHandle_t h;
+        CU(s, cudaIpcGetMemHandle(&h, s->base));
+        std::memcpy(ipc, &h, 64);
+    }
+    return EVOX_OK;
+}
+
+evox_status evox_cso_connect(evox_cso* s, int mode, const void* peers) {
+    evox_status st = check_cso(s);
+    if (st != EVOX_OK) return st;
+    if (!peers) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL peers");
+    if (mode != 0 && mode != 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
+    if (s->world > evox::kMaxPeers) return fail(EVOX_ERR_CONFIG, "world <= %d", evox::kMaxPeers);
+    if (s->t >= 0) return fail(EVOX_ERR_CONTRACT, "connect before the first step");
+    DevGuard g(s->device);
+    for (int r = 0; r < s->world; ++r) {
+        unsigned char* base = nullptr;
+        if (r == s->rank) {
+            base = static_cast<unsigned char*>(s->base);
+        } else if (mode == 0) {
+            base = static_cast<unsigned char*>(static_cast<void* const*>(peers)[r]);
+            if (!base) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL state pointer for rank %d", r);
+            cudaPointerAttributes at;
+            CU(s, cudaPointerGetAttributes(&at, base));
+            if (at.device != s->device) {
+                cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else if (e != cudaSuccess) return poison(s, EVOX_ERR_CUDA, "cudaDeviceEnablePeerAccess", e);
+            }
+        } else {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const uint8_t*>(peers) + 64 * r, 64);
+            void* p = nullptr;
+            CU(s, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            s->ipc_opened.push_back(p);
+            base = static_cast<unsigned char*>(p);
+        }
+        evox_cso probe;  // rank r's layout: the same carving with its own shard size
+        probe.world = s->world;
+        probe.ld = s->ld;
+        probe.phi = s->phi;
+        shard(s->pop, s->world, r, &probe.row0, &probe.rows);
+        Carver c;
+        cso_layout(&probe, c);
+        c.assign(base);
+        s->pX[r] = probe.X;
+        s->pf[r] = probe.f;
+        s->pmbox[r] = probe.mbox;
+        s->prow0[r] = probe.row0;
+    }
+    st = ensure_hist(s, 1 << 16);  // a step must never synchronise (single-process groups)
+    if (st != EVOX_OK) return st;
+    if (const char* ms = std::getenv("EVOX_PEER_TIMEOUT_MS"))
+        s->peer_timeout_ns = (unsigned long long)std::strtoull(ms, nullptr, 10) * 1000000ull;
+    s->peer = true;
+    for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
+    s->graphs.clear();
+    for (int p = 0; p < 5; ++p) s->gen_grid[p] = evox::cso_gen_grid(p, s->args(), s->device);
+    return EVOX_OK;
+}
+
 evox_status evox_cso_set_timing(evox_cso* s, int enable) {
     evox_status st = check_cso(s);
     if (st != EVOX_OK) return st;
@@ -1353,6 +1472,8 @@ evox_status evox_cso_kernel_time(evox_cso* s, double* total_ms, int64_t* gens, i
 evox_status evox_cso_destroy(evox_cso* s) {
     if (!s) return EVOX_OK;
     DevGuard g(s->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
     if (s->keybuf) cudaFree(s->keybuf);
     base_release(s);
     delete s;

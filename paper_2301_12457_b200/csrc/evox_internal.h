@@ -74,6 +74,16 @@ struct CsoArgs {
     Ctl* ctl;
     int rank, world;
     int exchange;  // 1: per-generation keys go to hkeys for one NCCL min-reduction per call
+    // global pairing across shards (evox_cso_connect): pairing blocks may straddle
+    // shards; every rank's X and f (own included) and the mailboxes of the
+    // per-generation barrier + global minimum.  Not connected: one table entry
+    // (our own shard).
+    int peer, nsh;
+    float* pX[kMaxPeers];
+    float* pf[kMaxPeers];
+    long long prow0[kMaxPeers + 1];
+    unsigned char* mbox[kMaxPeers];
+    unsigned long long peer_timeout_ns;
 };
 
 // DE/rand/1/bin (R-14).  The population lives in two buffers; sel[p][i] says

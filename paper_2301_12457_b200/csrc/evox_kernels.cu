@@ -514,6 +514,38 @@ __device__ void peer_exchange(const PsoArgs& a, unsigned long long key, unsigned
     }
 }
 
+// End-of-generation barrier of a row-sharded population whose shards read each
+// other (DE donors, CSO cross-shard pairs): publish this rank's min key in every
+// rank's mailbox (slot[par][rank] = {flag, key}), wait for all, return the
+// global min.  No rank starts generation t+1 (which may overwrite rows peers
+// read in generation t) before every rank finished generation t.  One thread.
+__device__ unsigned long long peer_min(unsigned char* const* mbox, int rank, int world,
+                                       unsigned long long timeout_ns, Ctl* ctl,
+                                       unsigned long long key, unsigned long long t_new) {
+    const int par = (int)(t_new & 1);
+    const unsigned long long flag = t_new + 1;
+    const long long my = ((long long)par * world + rank) * 16;
+    for (int w = 0; w < world; ++w) *reinterpret_cast<unsigned long long*>(mbox[w] + my + 8) = key;
+    __threadfence_system();
+    for (int w = 0; w < world; ++w)
+        st_release_sys(reinterpret_cast<unsigned long long*>(mbox[w] + my), flag);
+    unsigned long long kmin = ~0ull;
+    const unsigned long long t0 = globaltimer_ns();
+    for (int w = 0; w < world; ++w) {
+        const unsigned char* slot = mbox[rank] + ((long long)par * world + w) * 16;
+        while (ld_acquire_sys(reinterpret_cast<const unsigned long long*>(slot)) != flag) {
+            if (globaltimer_ns() - t0 > timeout_ns) {
+                ctl->err = 1;
+                break;
+            }
+            __nanosleep(256);
+        }
+        const unsigned long long kw = __ldcg(reinterpret_cast<const unsigned long long*>(slot + 8));
+        kmin = kw < kmin ? kw : kmin;
+    }
+    return kmin;
+}
+
 // In the last CTA: gbest update (strict, R-5), hist, or the winner record for
 // the exchange.  `t_new` is the index of the population just evaluated.
 __device__ void pso_finalize(const PsoArgs& a, unsigned long long key, unsigned long long t_new) {
@@ -1172,7 +1204,9 @@ struct MoverCso {
 __device__ void cso_finalize(const CsoArgs& a, unsigned long long key, unsigned long long t_new) {
     if (threadIdx.x == 0) {
         Ctl* ctl = a.ctl;
-        if (a.exchange) {
+        if (a.peer) key = peer_min(a.mbox, a.rank, a.world, a.peer_timeout_ns, ctl, key, t_new);
+        ctl->min_key = key;
+        if (a.exchange && !a.peer) {
             ctl->hkeys[t_new] = key;
         } else {
             ctl->hist[t_new] = key != ~0ull ? unord_f32((uint32_t)(key >> 32))
@@ -1191,13 +1225,32 @@ struct CsoItem {
     bool valid;
 };
 
+__device__ __forceinline__ int cso_owner(const CsoArgs& a, long long r) {
+    int w = 0;
+    while (w + 1 < a.nsh && r >= a.prow0[w + 1]) ++w;
+    return w;
+}
+__device__ __forceinline__ float cso_f(const CsoArgs& a, long long r) {
+    const int w = cso_owner(a, r);
+    return a.pf[w][r - a.prow0[w]];
+}
+// Blocks this rank scans: its own (aligned shards) or all of them (global pairing).
+__device__ __forceinline__ long long cso_blk0(const CsoArgs& a) { return a.peer ? 0 : a.row0 / a.B; }
+__device__ __forceinline__ long long cso_nitems(const CsoArgs& a) {
+    const long long blk0 = cso_blk0(a);
+    const long long end = a.peer ? a.pop : a.row0 + a.rows;
+    return ((end + a.B - 1) / a.B - blk0) * ((a.B + 1) / 2);
+}
+
+// Item `it`: its pair (or the unpaired member), the decision, and whether this
+// rank does the work (it owns the loser / the unpaired member).
 __device__ __forceinline__ CsoItem cso_item(const CsoArgs& a, long long it, uint32_t t) {
     CsoItem r;
     r.valid = false;
     r.gl = -1;
     r.gw = 0;
     r.fw = 0.f;
-    const long long blk0 = a.row0 / a.B;
+    const long long blk0 = cso_blk0(a);
     const long long ipb = (a.B + 1) / 2;
     const long long bl = it / ipb, p = it - bl * ipb;
     const long long blk = blk0 + bl;
@@ -1207,21 +1260,26 @@ __device__ __forceinline__ CsoItem cso_item(const CsoArgs& a, long long it, uint
     if (p >= (Bb + 1) / 2) return r;
     CsoPerm perm;
     perm.init((uint32_t)blk, t, (uint32_t)Bb, a.rk);
-    r.valid = true;
+    const long long lo = a.row0, hi = a.row0 + a.rows;  // this rank's rows
     if (2 * p + 1 >= Bb) {  // odd block: unpaired member passes unchanged
         r.gw = base + perm((uint32_t)(Bb - 1));
-        r.fw = a.f[r.gw - a.row0];
+        r.valid = r.gw >= lo && r.gw < hi;
+        if (r.valid) r.fw = a.f[r.gw - a.row0];
         return r;
     }
     const long long gi = base + perm((uint32_t)(2 * p));
     const long long gk = base + perm((uint32_t)(2 * p + 1));
-    const float fi = a.f[gi - a.row0], fk = a.f[gk - a.row0];
+    const bool li = gi >= lo && gi < hi, lk = gk >= lo && gk < hi;
+    if (!li && !lk) return r;  // neither member is ours
+    const float fi = li ? a.f[gi - a.row0] : cso_f(a, gi);
+    const float fk = lk ? a.f[gk - a.row0] : cso_f(a, gk);
     const float oi = fi != fi ? __int_as_float(0x7f800000) : fi;
     const float ok = fk != fk ? __int_as_float(0x7f800000) : fk;
     const bool i_wins = oi < ok || (oi == ok && gi < gk);
     r.gw = i_wins ? gi : gk;
     r.gl = i_wins ? gk : gi;
     r.fw = i_wins ? fi : fk;
+    r.valid = i_wins ? lk : li;  // the loser's owner updates it
     return r;
 }
 
@@ -1235,9 +1293,7 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_cso_gen(CsoArgs a) {
     const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
     const RowMap<G> m(a.ld >> 2);
     const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
-    const long long blk0 = a.row0 / a.B;
-    const long long nblk = (a.row0 + a.rows + a.B - 1) / a.B - blk0;
-    const long long items = nblk * ((a.B + 1) / 2);
+    const long long items = cso_nitems(a);
     NoPrefetch pf;
     unsigned long long best = ~0ull;
     const long long seg_off = m.qb * 16, seg_bytes = (m.qe - m.qb) * 16;
@@ -1260,7 +1316,8 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_cso_gen(CsoArgs a) {
             const long long ol = (ci_nxt.gl - a.row0) * a.ld * 4 + seg_off;
             prefetch_l2(X + ol, seg_bytes);
             prefetch_l2(reinterpret_cast<const char*>(a.V) + ol, seg_bytes);
-            prefetch_l2(X + (ci_nxt.gw - a.row0) * a.ld * 4 + seg_off, seg_bytes);
+            if (ci_nxt.gw >= a.row0 && ci_nxt.gw < a.row0 + a.rows)  // local winners only
+                prefetch_l2(X + (ci_nxt.gw - a.row0) * a.ld * 4 + seg_off, seg_bytes);
         }
         CsoItem ci_nn;
         ci_nn.valid = false;
@@ -1271,7 +1328,12 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_cso_gen(CsoArgs a) {
         const long long lrow = pair ? ci.gl - a.row0 : 0, wrow = pair ? ci.gw - a.row0 : 0;
         mv.Xl = reinterpret_cast<float4*>(a.X + lrow * a.ld);
         mv.Vl = reinterpret_cast<float4*>(a.V + lrow * a.ld);
-        mv.Xw = reinterpret_cast<const float4*>(a.X + wrow * a.ld);
+        if (pair && (ci.gw < a.row0 || ci.gw >= a.row0 + a.rows)) {  // winner on a peer GPU
+            const int w = cso_owner(a, ci.gw);
+            mv.Xw = reinterpret_cast<const float4*>(a.pX[w] + (ci.gw - a.prow0[w]) * a.ld);
+        } else {
+            mv.Xw = reinterpret_cast<const float4*>(a.X + wrow * a.ld);
+        }
         mv.row_g = (uint32_t)(pair ? ci.gl : 0);
         mv.t = (uint32_t)t;
         Fit<P> acc;
@@ -1292,7 +1354,7 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_cso_gen(CsoArgs a) {
         ci_nxt = ci_nn;
     }
     unsigned long long key;
-    if (grid_argmin(a.ctl, best, &key)) cso_finalize(a, key, t + 1);
+    if (grid_argmin(a.ctl, best, &key, a.peer != 0)) cso_finalize(a, key, t + 1);
 }
 
 // Generation 0 (after the evaluation of X0): population minimum -> hist[0].
@@ -1304,7 +1366,7 @@ __global__ void __launch_bounds__(256) k_cso_tell0(CsoArgs a) {
         best = k < best ? k : best;
     }
     unsigned long long key;
-    if (grid_argmin(a.ctl, best, &key)) cso_finalize(a, key, 0);
+    if (grid_argmin(a.ctl, best, &key, a.peer != 0)) cso_finalize(a, key, 0);
 }
 
 __global__ void k_cso_init(CsoArgs a) {
@@ -1447,42 +1509,12 @@ __device__ __forceinline__ const float4* de_row(const DeArgs& a, long long r, in
     return reinterpret_cast<const float4*>(a.pbuf[w][s] + lr * a.ld);
 }
 
-// End-of-generation barrier of the sharded DE: publish this rank's min key in
-// every rank's mailbox (slot[par][rank] = {flag, key}), wait for all, return the
-// global min.  No rank starts generation t+1 (which may overwrite rows peers
-// read as donors in generation t) before every rank finished generation t.
-__device__ unsigned long long de_peer_min(const DeArgs& a, unsigned long long key,
-                                          unsigned long long t_new) {
-    const int par = (int)(t_new & 1);
-    const unsigned long long flag = t_new + 1;
-    const long long my = ((long long)par * a.world + a.rank) * 16;
-    for (int w = 0; w < a.world; ++w)
-        *reinterpret_cast<unsigned long long*>(a.mbox[w] + my + 8) = key;
-    __threadfence_system();
-    for (int w = 0; w < a.world; ++w)
-        st_release_sys(reinterpret_cast<unsigned long long*>(a.mbox[w] + my), flag);
-    unsigned long long kmin = ~0ull;
-    const unsigned long long t0 = globaltimer_ns();
-    for (int w = 0; w < a.world; ++w) {
-        const unsigned char* slot = a.mbox[a.rank] + ((long long)par * a.world + w) * 16;
-        while (ld_acquire_sys(reinterpret_cast<const unsigned long long*>(slot)) != flag) {
-            if (globaltimer_ns() - t0 > a.peer_timeout_ns) {
-                a.ctl->err = 1;
-                break;
-            }
-            __nanosleep(256);
-        }
-        const unsigned long long kw = __ldcg(reinterpret_cast<const unsigned long long*>(slot + 8));
-        kmin = kw < kmin ? kw : kmin;
-    }
-    return kmin;
-}
 
 __device__ __forceinline__ void de_finalize(const DeArgs& a, unsigned long long key,
                                             unsigned long long t_new) {
     if (threadIdx.x == 0) {
         Ctl* ctl = a.ctl;
-        if (a.peer) key = de_peer_min(a, key, t_new);
+        if (a.peer) key = peer_min(a.mbox, a.rank, a.world, a.peer_timeout_ns, ctl, key, t_new);
         ctl->hist[t_new] = key != ~0ull ? unord_f32((uint32_t)(key >> 32)) : __int_as_float(0x7f800000);
         ctl->min_key = key;
         ctl->gen_key = ~0ull;
@@ -1828,9 +1860,9 @@ cudaError_t launch_cso_tell0(const CsoArgs& a, cudaStream_t st) {
 }
 
 static long long cso_items(const CsoArgs& a) {
-    const long long blk0 = a.row0 / a.B;
-    const long long nblk = (a.row0 + a.rows + a.B - 1) / a.B - blk0;
-    return nblk * ((a.B + 1) / 2);
+    const long long blk0 = a.peer ? 0 : a.row0 / a.B;
+    const long long end = a.peer ? a.pop : a.row0 + a.rows;
+    return ((end + a.B - 1) / a.B - blk0) * ((a.B + 1) / 2);
 }
 
 int cso_gen_grid(int problem, const CsoArgs& a, int device) {

@@ -103,6 +103,8 @@ SIGNATURES = {
     "evox_cso_sync": ([_p], _i),
     "evox_cso_destroy": ([_p], _i),
     "evox_cso_set_timing": ([_p, _i], _i),
+    "evox_cso_state": ([_p, _PP, _p], _i),
+    "evox_cso_connect": ([_p, _i, _p], _i),
     "evox_cso_kernel_time": ([_p, ctypes.POINTER(ctypes.c_double), _PI64, _PI64, _i], _i),
     "evox_de_workspace_bytes": ([_i64, _i64, _PSZ], _i),
     "evox_de_init": ([_i64, _i64, _p, _p, _f32, _f32, _u64, _p, _PP], _i),
@@ -449,6 +451,24 @@ class CSO(_Handle):
 
     def step(self, problem, n_gens: int = 1):
         _check(lib().evox_cso_step(self._h, problem_id(problem), int(n_gens)))
+
+    def state_base(self) -> int:
+        p = ctypes.c_void_p()
+        _check(lib().evox_cso_state(self._h, ctypes.byref(p), None))
+        return p.value
+
+    def state_ipc(self) -> bytes:
+        buf = (ctypes.c_uint8 * 64)()
+        _check(lib().evox_cso_state(self._h, None, buf))
+        return bytes(buf)
+
+    def connect_local(self, bases):
+        arr = (ctypes.c_void_p * len(bases))(*[int(b) for b in bases])
+        _check(lib().evox_cso_connect(self._h, 0, arr))
+
+    def connect_ipc(self, handles):
+        buf = ctypes.create_string_buffer(b"".join(bytes(h) for h in handles))
+        _check(lib().evox_cso_connect(self._h, 1, buf))
 
 
 class DE(_Handle):

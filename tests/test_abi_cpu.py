@@ -93,11 +93,13 @@ def test_cso_init_validation():
     o.world, o.rank = 2, 0
     nid = (ctypes.c_uint8 * 128)()
     o.nccl_id = ctypes.addressof(nid)
-    # shards must hold whole pairing blocks: pop 100, W 2, B 30 -> 50 % 30 != 0
-    assert L.evox_cso_init(100, 4, lb.ctypes.data, ub.ctypes.data, 0.0, 30, 0, ctypes.byref(o),
+    # blocks straddling shards need peer connection: not with world > 8 or a workspace
+    o.world = 9
+    assert L.evox_cso_init(90, 4, lb.ctypes.data, ub.ctypes.data, 0.0, 90, 0, ctypes.byref(o),
                            ctypes.byref(h)) == E.CONFIG
+    o.world = 2
     assert L.evox_cso_init(100, 4, lb.ctypes.data, ub.ctypes.data, 0.5, 25, 0, ctypes.byref(o),
-                           ctypes.byref(h)) == E.CONFIG
+                           ctypes.byref(h)) == E.CONFIG  # phi != 0 with world > 1
 
 
 def test_eval_validation():

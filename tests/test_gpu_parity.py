@@ -566,3 +566,49 @@ def test_eval_nonfinite_rows():
     assert np.isinf(f[1]) and np.isnan(f[2])
     ref = O.evaluate("sphere", X[[0, 3]])
     assert_fitness(f[[0, 3]], ref, "finite rows")
+
+
+# ------------------------------------------- CSO global pairing across shards
+def _cso_group(W, N, D, lb, ub, B, seed):
+    hs = [ev.CSO(N, D, lb, ub, block=B, seed=seed, rank=r, world=W, stream=torch.cuda.Stream())
+          for r in range(W)]
+    bases = [h.state_base() for h in hs]
+    for h in hs:
+        h.connect_local(bases)
+    return hs
+
+
+@pytest.mark.parametrize("W,N,D,B,problem", [(2, 64, 33, 64, "rastrigin"),
+                                             (3, 50, 100, 50, "ackley"),
+                                             (4, 97, 1000, 30, "sphere"),
+                                             (8, 203, 20, 203, "griewank"),
+                                             (2, 10, 4099, 7, "rosenbrock")])
+def test_cso_global_pairing_sharded_equals_single(W, N, D, B, problem):
+    """Pairing blocks straddle shards (B = pop is global pairing): losers are updated by
+    their owner from winner rows read through peer memory -- bitwise the W = 1 run."""
+    lb, ub = WL.BOUNDS[problem]
+    ref = ev.CSO(N, D, lb, ub, block=B, seed=4)
+    ref.step(problem, 25)
+    hs = _cso_group(W, N, D, lb, ub, B, 4)
+    for h in hs:
+        h.step(problem, 0)
+    for _ in range(5):
+        for h in hs:
+            h.step(problem, 5)
+    for h in hs:
+        h.sync()
+    X = np.concatenate([h.view("X").cpu().numpy()[:, :D] for h in hs])
+    F = np.concatenate([h.view("F").cpu().numpy() for h in hs])
+    assert np.array_equal(X, ref.view("X").cpu().numpy()[:, :D])
+    assert np.array_equal(F, ref.view("F").cpu().numpy())
+    rb = ref.best()
+    for h in hs:
+        assert np.array_equal(h.history(), ref.history())
+        b = h.best()
+        assert b[0] == rb[0] and b[1] == rb[1] and np.array_equal(b[2], rb[2])
+
+
+def test_cso_straddling_blocks_require_connect():
+    h = ev.CSO(30, 4, -1, 1, block=30, rank=0, world=2)
+    with pytest.raises(E.ContractError):
+        h.step("sphere", 1)
