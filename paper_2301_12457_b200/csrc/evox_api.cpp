@@ -1006,19 +1006,21 @@ struct evox_cso : Base {
     bool peer = false;
     unsigned long long peer_timeout_ns = 60ull * 1000 * 1000 * 1000;
     float* pX[evox::kMaxPeers] = {};
-    float* pf[evox::kMaxPeers] = {};
+    float* pf[evox::kMaxPeers][2] = {};
     unsigned char* pmbox[evox::kMaxPeers] = {};
     long long prow0[evox::kMaxPeers + 1] = {};
     std::vector<void*> ipc_opened;
     unsigned char* mbox = nullptr;
-    float *X = nullptr, *V = nullptr, *f = nullptr, *xbar = nullptr;
+    float *X = nullptr, *V = nullptr, *xbar = nullptr;
+    float* f2[2] = {nullptr, nullptr};  // fitness by generation parity
+    float* fcur() const { return f2[(t < 0 ? 0 : t) & 1]; }
     double* colpart = nullptr;
     unsigned long long* keybuf = nullptr;
     int gen_grid[5] = {0, 0, 0, 0, 0};
     CsoArgs args() const {
         CsoArgs a;
         std::memset(&a, 0, sizeof a);
-        a.X = X; a.V = V; a.f = f;
+        a.X = X; a.V = V; a.f2[0] = f2[0]; a.f2[1] = f2[1];
         a.lb = lb_d; a.ub = ub_d; a.lb0 = lb[0]; a.ub0 = ub[0];
         a.uniform_bounds = uniform ? 1 : 0;
         a.rows = rows; a.row0 = row0; a.D = dim; a.ld = ld; a.pop = pop;
@@ -1036,7 +1038,8 @@ struct evox_cso : Base {
             a.nsh = world;
             for (int r = 0; r < world; ++r) {
                 a.pX[r] = pX[r];
-                a.pf[r] = pf[r];
+                a.pf[r][0] = pf[r][0];
+                a.pf[r][1] = pf[r][1];
                 a.mbox[r] = pmbox[r];
                 a.prow0[r] = prow0[r];
             }
@@ -1044,7 +1047,8 @@ struct evox_cso : Base {
         } else {  // one table entry: our own shard
             a.nsh = 1;
             a.pX[0] = X;
-            a.pf[0] = f;
+            a.pf[0][0] = f2[0];
+            a.pf[0][1] = f2[1];
             a.mbox[0] = mbox;
             a.prow0[0] = row0;
             a.prow0[1] = row0 + rows;
@@ -1059,7 +1063,8 @@ void cso_layout(evox_cso* s, Carver& c) {
     const size_t mat = sizeof(float) * (size_t)s->rows * (size_t)s->ld;
     c.add(&s->X, mat);
     c.add(&s->V, mat);
-    c.add(&s->f, sizeof(float) * s->rows);
+    c.add(&s->f2[0], sizeof(float) * s->rows);
+    c.add(&s->f2[1], sizeof(float) * s->rows);
     c.add(&s->lb_d, sizeof(float) * s->ld);
     c.add(&s->ub_d, sizeof(float) * s->ld);
     c.add(&s->ctl, sizeof(Ctl));
@@ -1143,6 +1148,8 @@ evox_status evox_cso_init(int64_t pop, int64_t dim, const float* lb, const float
         DevGuard g(s->device);
         cudaError_t e = evox::launch_cso_init(s->args(), s->stream);
         if (e == cudaSuccess) e = cudaMemsetAsync(s->xbar, 0, sizeof(float) * s->ld, s->stream);
+        if (e == cudaSuccess)  // peer-barrier flags start at 0 ("nothing published")
+            e = cudaMemsetAsync(s->mbox, 0, (size_t)32 * (s->world > 1 ? s->world : 1), s->stream);
         if (e == cudaSuccess) e = cudaMalloc(&s->keybuf, sizeof(unsigned long long));
         if (e != cudaSuccess) st = poison(s, EVOX_ERR_CUDA, "cso init", e);
         for (int p = 0; p < 5 && st == EVOX_OK; ++p)
@@ -1180,7 +1187,7 @@ evox_status evox_cso_step(evox_cso* s, evox_problem problem, int64_t n_gens) {
     const CsoArgs a = s->args();
     int64_t first = t0 + 1;  // first hist index written by this call
     if (s->t < 0) {
-        CU(s, evox::launch_eval((int)problem, s->X, s->rows, s->dim, s->ld, s->f, s->stream));
+        CU(s, evox::launch_eval((int)problem, s->X, s->rows, s->dim, s->ld, s->f2[0], s->stream));
         CU(s, evox::launch_cso_tell0(a, s->stream));
         s->t = 0;
         first = 0;
@@ -1220,7 +1227,7 @@ evox_status evox_cso_best(evox_cso* s, float* fit, int64_t* global_index, float*
     DevGuard g(s->device);
     const evox::NcclApi* api = (s->comm && !s->peer) ? evox::nccl_api(nullptr) : nullptr;
     if (!s->peer) {
-        CU(s, evox::launch_argmin_rows(s->f, s->rows, s->row0, s->keybuf, s->stream));
+        CU(s, evox::launch_argmin_rows(s->fcur(), s->rows, s->row0, s->keybuf, s->stream));
         if (api)
             NC(s, api->AllReduce(s->keybuf, s->keybuf, 1, ncclUint64, ncclMin, s->comm, s->stream));
     }
@@ -1288,7 +1295,7 @@ evox_status evox_cso_view(evox_cso* s, int field, void** dev, int64_t* rows, int
     switch (field) {
         case EVOX_FIELD_X: *dev = s->X; break;
         case EVOX_FIELD_V: *dev = s->V; break;
-        case EVOX_FIELD_F: *dev = s->f; l = 1; break;
+        case EVOX_FIELD_F: *dev = s->fcur(); l = 1; break;
         default: return fail(EVOX_ERR_INVALID_ARGUMENT, "field %d not available for CSO", field);
     }
     if (rows) *rows = r;
@@ -1334,7 +1341,7 @@ evox_status evox_cso_save(evox_cso* s, void* host_blob, size_t cap, size_t* used
     p += sizeof h;
     CU(s, cudaMemcpy(p, s->X, mat, cudaMemcpyDeviceToHost)); p += mat;
     CU(s, cudaMemcpy(p, s->V, mat, cudaMemcpyDeviceToHost)); p += mat;
-    CU(s, cudaMemcpy(p, s->f, 4 * s->rows, cudaMemcpyDeviceToHost)); p += 4 * s->rows;
+    CU(s, cudaMemcpy(p, s->fcur(), 4 * s->rows, cudaMemcpyDeviceToHost)); p += 4 * s->rows;
     if (T > 0) CU(s, cudaMemcpy(p, s->hist, 4 * T, cudaMemcpyDeviceToHost));
     return EVOX_OK;
 }
@@ -1362,7 +1369,8 @@ evox_status evox_cso_load(evox_cso* s, const void* host_blob, size_t size) {
     const char* p = static_cast<const char*>(host_blob) + sizeof h;
     CU(s, cudaMemcpy(s->X, p, mat, cudaMemcpyHostToDevice)); p += mat;
     CU(s, cudaMemcpy(s->V, p, mat, cudaMemcpyHostToDevice)); p += mat;
-    CU(s, cudaMemcpy(s->f, p, 4 * s->rows, cudaMemcpyHostToDevice)); p += 4 * s->rows;
+    CU(s, cudaMemcpy(s->f2[(h.t < 0 ? 0 : h.t) & 1], p, 4 * s->rows, cudaMemcpyHostToDevice));
+    p += 4 * s->rows;
     if (T > 0) CU(s, cudaMemcpy(s->hist, p, 4 * T, cudaMemcpyHostToDevice));
     Ctl c;
     CU(s, cudaMemcpy(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost));
@@ -1428,7 +1436,8 @@ evox_status evox_cso_connect(evox_cso* s, int mode, const void* peers) {
         cso_layout(&probe, c);
         c.assign(base);
         s->pX[r] = probe.X;
-        s->pf[r] = probe.f;
+        s->pf[r][0] = probe.f2[0];
+        s->pf[r][1] = probe.f2[1];
         s->pmbox[r] = probe.mbox;
         s->prow0[r] = probe.row0;
     }
@@ -1615,6 +1624,8 @@ evox_status evox_de_init(int64_t pop, int64_t dim, const float* lb, const float*
     if (st == EVOX_OK) {
         DevGuard g(s->device);
         cudaError_t e = evox::launch_de_init(s->args(), s->stream);
+        if (e == cudaSuccess)  // peer-barrier flags start at 0 ("nothing published")
+            e = cudaMemsetAsync(s->mbox, 0, (size_t)32 * (s->world > 1 ? s->world : 1), s->stream);
         if (e != cudaSuccess) st = poison(s, EVOX_ERR_CUDA, "de init", e);
         for (int p = 0; p < 5 && st == EVOX_OK; ++p)
             s->gen_grid[p] = evox::de_gen_grid(p, s->ld, s->rows, s->device);

@@ -60,7 +60,8 @@ struct PsoArgs {
 struct CsoArgs {
     float* X;
     float* V;
-    float* f;
+    float* f2[2];  // fitness by generation parity: read f2[t&1], write f2[(t+1)&1] (pairs
+                   // straddling shards are decided by both owners from generation-t values)
     const float* lb;
     const float* ub;
     float lb0, ub0;
@@ -80,7 +81,7 @@ struct CsoArgs {
     // (our own shard).
     int peer, nsh;
     float* pX[kMaxPeers];
-    float* pf[kMaxPeers];
+    float* pf[kMaxPeers][2];
     long long prow0[kMaxPeers + 1];
     unsigned char* mbox[kMaxPeers];
     unsigned long long peer_timeout_ns;

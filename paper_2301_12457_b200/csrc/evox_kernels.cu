@@ -1222,7 +1222,8 @@ __device__ void cso_finalize(const CsoArgs& a, unsigned long long key, unsigned 
 struct CsoItem {
     long long gw, gl;  // winner, loser global rows (gl < 0: unpaired member gw passes)
     float fw;
-    bool valid;
+    bool valid;  // this rank updates the loser (or owns the unpaired member)
+    bool wl;     // the winner (or the unpaired member) is one of this rank's rows
 };
 
 __device__ __forceinline__ int cso_owner(const CsoArgs& a, long long r) {
@@ -1230,9 +1231,9 @@ __device__ __forceinline__ int cso_owner(const CsoArgs& a, long long r) {
     while (w + 1 < a.nsh && r >= a.prow0[w + 1]) ++w;
     return w;
 }
-__device__ __forceinline__ float cso_f(const CsoArgs& a, long long r) {
+__device__ __forceinline__ float cso_f(const CsoArgs& a, long long r, int p) {
     const int w = cso_owner(a, r);
-    return a.pf[w][r - a.prow0[w]];
+    return a.pf[w][p][r - a.prow0[w]];
 }
 // Blocks this rank scans: its own (aligned shards) or all of them (global pairing).
 __device__ __forceinline__ long long cso_blk0(const CsoArgs& a) { return a.peer ? 0 : a.row0 / a.B; }
@@ -1247,6 +1248,7 @@ __device__ __forceinline__ long long cso_nitems(const CsoArgs& a) {
 __device__ __forceinline__ CsoItem cso_item(const CsoArgs& a, long long it, uint32_t t) {
     CsoItem r;
     r.valid = false;
+    r.wl = false;
     r.gl = -1;
     r.gw = 0;
     r.fw = 0.f;
@@ -1261,25 +1263,29 @@ __device__ __forceinline__ CsoItem cso_item(const CsoArgs& a, long long it, uint
     CsoPerm perm;
     perm.init((uint32_t)blk, t, (uint32_t)Bb, a.rk);
     const long long lo = a.row0, hi = a.row0 + a.rows;  // this rank's rows
+    const int par = (int)(t & 1);
+    const float* f = a.f2[par];
     if (2 * p + 1 >= Bb) {  // odd block: unpaired member passes unchanged
         r.gw = base + perm((uint32_t)(Bb - 1));
         r.valid = r.gw >= lo && r.gw < hi;
-        if (r.valid) r.fw = a.f[r.gw - a.row0];
+        r.wl = r.valid;
+        if (r.valid) r.fw = f[r.gw - a.row0];
         return r;
     }
     const long long gi = base + perm((uint32_t)(2 * p));
     const long long gk = base + perm((uint32_t)(2 * p + 1));
     const bool li = gi >= lo && gi < hi, lk = gk >= lo && gk < hi;
     if (!li && !lk) return r;  // neither member is ours
-    const float fi = li ? a.f[gi - a.row0] : cso_f(a, gi);
-    const float fk = lk ? a.f[gk - a.row0] : cso_f(a, gk);
+    const float fi = li ? f[gi - a.row0] : cso_f(a, gi, par);
+    const float fk = lk ? f[gk - a.row0] : cso_f(a, gk, par);
     const float oi = fi != fi ? __int_as_float(0x7f800000) : fi;
     const float ok = fk != fk ? __int_as_float(0x7f800000) : fk;
     const bool i_wins = oi < ok || (oi == ok && gi < gk);
     r.gw = i_wins ? gi : gk;
     r.gl = i_wins ? gk : gi;
     r.fw = i_wins ? fi : fk;
-    r.valid = i_wins ? lk : li;  // the loser's owner updates it
+    r.valid = i_wins ? lk : li;  // the loser's owner updates it (and contributes the key)
+    r.wl = i_wins ? li : lk;     // the winner's owner carries its fitness to the next parity
     return r;
 }
 
@@ -1303,8 +1309,8 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_cso_gen(CsoArgs a) {
     // to follow).  Pairs are disjoint, so no other item of this generation
     // writes the fitness read here.
     CsoItem ci_cur, ci_nxt;
-    ci_cur.valid = false;
-    ci_nxt.valid = false;
+    ci_cur.valid = ci_cur.wl = false;
+    ci_nxt.valid = ci_nxt.wl = false;
     if (m.first < items) ci_cur = cso_item(a, m.first, (uint32_t)t);
     if (m.first + m.stride < items) ci_nxt = cso_item(a, m.first + m.stride, (uint32_t)t);
     for (long long k = 0;; ++k) {
@@ -1320,7 +1326,7 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_cso_gen(CsoArgs a) {
                 prefetch_l2(X + (ci_nxt.gw - a.row0) * a.ld * 4 + seg_off, seg_bytes);
         }
         CsoItem ci_nn;
-        ci_nn.valid = false;
+        ci_nn.valid = ci_nn.wl = false;
         if (it + 2 * m.stride < items) ci_nn = cso_item(a, it + 2 * m.stride, (uint32_t)t);
         const CsoItem ci = ci_cur;
         const bool pair = ci.valid && ci.gl >= 0;
@@ -1341,14 +1347,18 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_cso_gen(CsoArgs a) {
         bool tv;
         walk_segment<P, G>(mv, m.qb, m.qe, a.D, pair, acc, hx, tx, tv, pf, htab);
         const float fl = reduce_row<P, G>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
-        if (m.leader && ci.valid) {
-            unsigned long long kk = make_key(ci.fw, ci.gw);
-            if (pair) {
-                a.f[ci.gl - a.row0] = fl;
-                const unsigned long long kl = make_key(fl, ci.gl);
-                kk = kl < kk ? kl : kk;
+        if (m.leader) {
+            float* fnext = a.f2[(t + 1) & 1];
+            if (ci.wl) fnext[ci.gw - a.row0] = ci.fw;  // winner / unpaired: unchanged
+            if (ci.valid) {
+                unsigned long long kk = make_key(ci.fw, ci.gw);
+                if (pair) {
+                    fnext[ci.gl - a.row0] = fl;
+                    const unsigned long long kl = make_key(fl, ci.gl);
+                    kk = kl < kk ? kl : kk;
+                }
+                best = kk < best ? kk : best;
             }
-            best = kk < best ? kk : best;
         }
         ci_cur = ci_nxt;
         ci_nxt = ci_nn;
@@ -1362,7 +1372,7 @@ __global__ void __launch_bounds__(256) k_cso_tell0(CsoArgs a) {
     unsigned long long best = ~0ull;
     for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < a.rows;
          r += (long long)gridDim.x * blockDim.x) {
-        const unsigned long long k = make_key(a.f[r], a.row0 + r);
+        const unsigned long long k = make_key(a.f2[0][r], a.row0 + r);
         best = k < best ? k : best;
     }
     unsigned long long key;
