@@ -266,7 +266,7 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nid = None
-    peer = world > 1 and cfg.algo == "pso" and args.exchange == "peer"
+    peer = world > 1 and cfg.algo in ("pso", "cso") and args.exchange == "peer"
     if world > 1 and not peer and cfg.algo != "de":
         buf = torch.zeros(128, dtype=torch.uint8, device=cdev)
         if rank == 0:
@@ -288,10 +288,17 @@ def main():
             dist.all_gather(allh, mine)
             h.connect_ipc([bytes(x.cpu().numpy().tobytes()) for x in allh])
             barrier()
+    elif cfg.algo == "cso":  # N>1: shards connected through IPC-mapped states (peer barrier)
+        h = ev.CSO(cfg.pop, cfg.dim, lb, ub, block=cfg.pop // 8 if cfg.pop % 16 == 0 else 0,
+                   seed=0, rank=rank, world=world, nccl_id=nid)
+        if world > 1 and args.exchange == "peer":
+            mine = torch.frombuffer(bytearray(h.state_ipc()), dtype=torch.uint8).to(cdev)
+            allh = [torch.zeros(64, dtype=torch.uint8, device=cdev) for _ in range(world)]
+            dist.all_gather(allh, mine)
+            h.connect_ipc([bytes(x.cpu().numpy().tobytes()) for x in allh])
+            barrier()
     else:
-        Cls = ev.PSO if cfg.algo == "pso" else ev.CSO
-        kw = {} if cfg.algo == "pso" else {"block": cfg.pop // 8 if cfg.pop % 16 == 0 else 0}
-        h = Cls(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world, nccl_id=nid, **kw)
+        h = ev.PSO(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world, nccl_id=nid)
     if peer:  # mailboxes of all ranks mapped into every rank through CUDA IPC
         mine = torch.frombuffer(bytearray(h.mailbox_ipc()), dtype=torch.uint8).to(cdev)
         allh = [torch.zeros(64, dtype=torch.uint8, device=cdev) for _ in range(world)]

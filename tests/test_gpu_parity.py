@@ -612,3 +612,27 @@ def test_cso_straddling_blocks_require_connect():
     h = ev.CSO(30, 4, -1, 1, block=30, rank=0, world=2)
     with pytest.raises(E.ContractError):
         h.step("sphere", 1)
+
+
+@pytest.mark.parametrize("problem,N,D", [("ackley", 200, 1000), ("rosenbrock", 300, 100),
+                                         ("griewank", 50, 4099), ("rastrigin", 70, 37),
+                                         ("sphere", 9, 40001)])
+def test_fused_fitness_equals_evaluate(problem, N, D, monkeypatch):
+    """the fitness the fused generation kernel computes from registers is
+    bitwise the standalone Problem.evaluate of the same population (same per-row
+    reduction order: a function of dim only)."""
+    lb, ub = WL.BOUNDS[problem]
+    monkeypatch.setenv("EVOX_NO_SMALL", "1")
+    pso = ev.PSO(N, D, lb, ub, seed=1)
+    pso.step(problem, 3)
+    X = pso.view("X")
+    f = ev.evaluate(problem, X.clone(), dim=D).cpu().numpy()
+    assert np.array_equal(f, pso.view("F").cpu().numpy())
+    cso = ev.CSO(N + N % 2, D, lb, ub, seed=1)
+    cso.step(problem, 2)
+    f = ev.evaluate(problem, cso.view("X").clone(), dim=D).cpu().numpy()
+    assert np.array_equal(f, cso.view("F").cpu().numpy())
+    de = ev.DE(N, D, lb, ub, seed=1)
+    de.step(problem, 2)
+    f = ev.evaluate(problem, de.view("X").clone(), dim=D).cpu().numpy()
+    assert np.array_equal(f, de.view("F").cpu().numpy())
