@@ -21,7 +21,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -69,54 +68,57 @@ def algorithmic_bytes(cfg, rows):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock, power and clock-event (throttle) reasons sampled DURING the timed region:
+    NVML every 2 ms plus one sample at start and one at stop (so even a sub-millisecond
+    region is bracketed); nvidia-smi polling as a fallback."""
+    BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.rows = []  # (sm_mhz, max_mhz, power_w, reasons bitmask)
+        self.stop_ev = threading.Event()
         self.th = None
+        self.nvml = None
+
+    def _sample(self):
+        n, h = self.nvml, self.h
+        try:
+            rs = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            rs = n.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.rows.append((n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM),
+                          n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM),
+                          n.nvmlDeviceGetPowerUsage(h) / 1000.0, int(rs)))
+
+    def _loop(self):
+        while not self.stop_ev.wait(0.002):
+            self._sample()
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._sample()
         except Exception:
-            self.proc = None
+            self.nvml = None
             return
-        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th = threading.Thread(target=self._loop, daemon=True)
         self.th.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
-
     def stop(self):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-        if self.th is not None:
-            self.th.join(timeout=2)
-        if not self.rows:
+        if self.nvml is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v == "Active"})
-        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "power_w_max": max(pw) if pw else None, "samples": len(self.rows)}
+        self.stop_ev.set()
+        self.th.join(timeout=2)
+        self._sample()
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for r in self.rows for bit, name in self.BITS.items() if r[3] & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "power_w_max": max(r[2] for r in self.rows),
+                "samples": len(self.rows), "source": "nvml, 2 ms + bracketing samples"}
 
 
 def ncu_traffic(cfg_name):
