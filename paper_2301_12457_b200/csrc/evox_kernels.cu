@@ -36,6 +36,9 @@ namespace {
 #ifndef EVOX_MINB
 #define EVOX_MINB 2
 #endif
+#ifndef EVOX_AHEAD
+#define EVOX_AHEAD 4  // mode-B prefetch window, in lane groups
+#endif
 constexpr int U = EVOX_U;          // max chunks in flight per lane group (register slots)
 constexpr int WARPS = 8;           // warps per CTA (256 threads) in every geometry
 constexpr long long MODE_A_MAX = 384;  // quads per warp-iteration prefetched whole (mode A)
@@ -678,7 +681,7 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen(PsoArgs a) {
     wp.ld_bytes = a.ld * 4;
     wp.qb = m.qb;
     wp.seg = seg;
-    wp.ahead = seg < 4 * G::GROUP ? seg : 4 * G::GROUP;
+    wp.ahead = seg < EVOX_AHEAD * G::GROUP ? seg : EVOX_AHEAD * G::GROUP;
     wp.on = !mode_a && lane == 0;
     wp.c = 0;
     unsigned long long best = ~0ull;
@@ -1547,26 +1550,57 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_de_gen(DeArgs a) {
     const unsigned char* sel = a.sel[p];
     NoPrefetch pf;
     unsigned long long best = ~0ull;
+    // The next target's donors and the buffer flags of its rows are resolved one
+    // iteration ahead: their loads (scattered bytes) land while this row streams,
+    // so the row loads of the next iteration are not behind a 2-deep dependent
+    // chain (indices -> flags -> rows).
+    uint32_t nr[3] = {0, 0, 0}, nsb = 0;
+    float nfx = 0.0f;
+    auto resolve = [&](long long rw, uint32_t r3[3], uint32_t& sb, float& fx) {
+        if (rw < a.rows) {
+            long long r[3];
+            de_indices(a, a.row0 + rw, (uint32_t)t, r);
+            r3[0] = (uint32_t)r[0];
+            r3[1] = (uint32_t)r[1];
+            r3[2] = (uint32_t)r[2];
+            int fl[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int w = de_owner(a, r[k]);
+                fl[k] = a.psel[w][p][r[k] - a.prow0[w]];
+            }
+            sb = (uint32_t)sel[rw] | ((uint32_t)fl[0] << 1) | ((uint32_t)fl[1] << 2) |
+                 ((uint32_t)fl[2] << 3);
+            fx = a.f[p][rw];
+        }
+    };
+    resolve(m.first, nr, nsb, nfx);
     for (long long it = 0;; ++it) {
         const long long wrow = m.wfirst + it * m.stride;
         if (wrow >= a.rows) break;
         const long long row = m.first + it * m.stride;
         const bool ok = row < a.rows;
+        const uint32_t cr0 = nr[0], cr1 = nr[1], cr2 = nr[2], csb = nsb;
+        const float cfx = nfx;
+        resolve(row + m.stride, nr, nsb, nfx);
         MoverDe<UNI> mv(a);
         int si = 0;
         float fx = 0.0f;
         if (ok) {
-            long long r[3];
-            de_indices(a, a.row0 + row, (uint32_t)t, r);  // GLOBAL donor rows
-            si = sel[row];
+            si = (int)(csb & 1u);
+            auto donor = [&](uint32_t r, int k) {
+                const int w = de_owner(a, r);
+                return reinterpret_cast<const float4*>(a.pbuf[w][(csb >> (k + 1)) & 1u] +
+                                                       ((long long)r - a.prow0[w]) * a.ld);
+            };
             mv.Xi = reinterpret_cast<const float4*>(a.buf[si] + row * a.ld);
-            mv.Xa = de_row(a, r[0], p);
-            mv.Xb = de_row(a, r[1], p);
-            mv.Xc = de_row(a, r[2], p);
+            mv.Xa = donor(cr0, 0);
+            mv.Xb = donor(cr1, 1);
+            mv.Xc = donor(cr2, 2);
             mv.Out = reinterpret_cast<float4*>(a.buf[si ^ 1] + row * a.ld);
             const uint4 jw = Philox::run(make_uint4(0u, (uint32_t)(a.row0 + row), (uint32_t)t, 9u), a.rk);
             mv.jrand = (long long)(((unsigned long long)jw.x * (unsigned long long)a.D) >> 32);
-            fx = a.f[p][row];
+            fx = cfx;
         } else {
             mv.Xi = mv.Xa = mv.Xb = mv.Xc = nullptr;
             mv.Out = nullptr;
