@@ -1514,13 +1514,6 @@ __device__ __forceinline__ int de_owner(const DeArgs& a, long long r) {
     while (w + 1 < a.world && r >= a.prow0[w + 1]) ++w;
     return w;
 }
-// Row r of the population at parity p, wherever it lives (peer memory over NVLink).
-__device__ __forceinline__ const float4* de_row(const DeArgs& a, long long r, int p) {
-    const int w = de_owner(a, r);
-    const long long lr = r - a.prow0[w];
-    const int s = a.psel[w][p][lr];
-    return reinterpret_cast<const float4*>(a.pbuf[w][s] + lr * a.ld);
-}
 
 
 __device__ __forceinline__ void de_finalize(const DeArgs& a, unsigned long long key,
