@@ -1,0 +1,39 @@
+"""Small runs of every kernel family for compute-sanitizer (memcheck/racecheck/synccheck)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2301_12457_b200 as ev  # noqa: E402
+
+torch.cuda.set_device(0)
+for D in (10, 100, 1003, 4099):
+    for p in ("sphere", "ackley", "rastrigin", "griewank", "rosenbrock"):
+        pso = ev.PSO(37, D, -5, 5, seed=1)
+        pso.step(p, 3)
+        X = pso.ask()
+        pso.tell(ev.evaluate(p, X.clone(), dim=D, stream=pso.stream))
+        pso.view("P")
+        pso.best()
+        cso = ev.CSO(40, D, -5, 5, block=10, seed=1)
+        cso.step(p, 3)
+        cso.best()
+        de = ev.DE(24, D, -5, 5, seed=1)
+        de.step(p, 3)
+        de.view("X")
+        de.best()
+os.environ["EVOX_NO_SMALL"] = "1"
+pso = ev.PSO(300, 1000, -5, 5, seed=2)   # multi-CTA generation kernel + grid argmin
+pso.step("ackley", 3)
+pso.best()
+hs = [ev.PSO(64, 100, -5, 5, seed=3, rank=r, world=2, stream=torch.cuda.Stream()) for r in range(2)]
+boxes = [h.mailbox()[0] for h in hs]
+for h in hs:
+    h.connect_local(boxes)
+for h in hs:
+    h.step("sphere", 3)
+for h in hs:
+    h.sync()
+print("sanitize run ok")
