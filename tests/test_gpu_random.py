@@ -84,14 +84,15 @@ def test_random_de(k, problem, N, D, seed):
     assert np.array_equal(de.view("X").cpu().numpy()[:, :D], X)
     f = de.view("F").cpu().numpy().copy()
     for t in range(4):
-        X0 = X.copy()
         de.step(problem, 1)
         O.de_generation(problem, X, f, F64, t, seed, lb, ub)
         Xg = de.view("X").cpu().numpy()[:, :D]
         fg = de.view("F").cpu().numpy()
         for i in np.nonzero((Xg != X).any(1))[0]:
+            # a flipped accept/reject: the GPU's row and the oracle's row (one of them the
+            # trial, the other the target) must be near-tied in fitness
             assert near_tie(float(O.evaluate(problem, Xg[i][None])[0]),
-                            float(O.evaluate(problem, X0[i][None])[0])), (t, i)
+                            float(O.evaluate(problem, X[i][None])[0])), (t, i)
         X = Xg.copy()
         assert_fitness(fg, O.evaluate(problem, Xg), f"DE t={t + 1}")
         f = fg.copy()
