@@ -39,6 +39,9 @@ namespace {
 #ifndef EVOX_AHEAD
 #define EVOX_AHEAD 4  // mode-B prefetch window, in lane groups
 #endif
+#ifndef EVOX_PF
+#define EVOX_PF 3  // tuning: bit 0 enables mode-A (next rows), bit 1 mode-B (window) prefetch
+#endif
 constexpr int U = EVOX_U;          // max chunks in flight per lane group (register slots)
 constexpr int WARPS = 8;           // warps per CTA (256 threads) in every geometry
 constexpr long long MODE_A_MAX = 384;  // quads per warp-iteration prefetched whole (mode A)
@@ -682,7 +685,7 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen(PsoArgs a) {
     wp.qb = m.qb;
     wp.seg = seg;
     wp.ahead = seg < EVOX_AHEAD * G::GROUP ? seg : EVOX_AHEAD * G::GROUP;
-    wp.on = !mode_a && lane == 0;
+    wp.on = !mode_a && lane == 0 && (EVOX_PF & 2);
     wp.c = 0;
     unsigned long long best = ~0ull;
     // pbest-pending flags one and two iterations ahead (imp[r] is rewritten only
@@ -697,7 +700,7 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen(PsoArgs a) {
         const bool ok = row < a.rows;
         const long long nxt = row + m.stride, nn = nxt + m.stride;
         const bool nxt_ok = nxt < a.rows;
-        if (mode_a) {
+        if (mode_a && (EVOX_PF & 1)) {
             // the warp's next rows, HBM -> L2 now (X, V contiguous; P per row unless pending)
             const long long wn = wrow + m.stride;
             if (lane == 0 && wn < a.rows) {
@@ -710,7 +713,7 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen(PsoArgs a) {
             if (m.sl == 0 && nxt_ok && !pend_nxt)
                 prefetch_l2(reinterpret_cast<const char*>(a.P) + nxt * a.ld * 4 + m.qb * 16,
                             seg * 16);
-        } else {
+        } else if (!mode_a) {
             wp.row = row;
             wp.nxt = nxt_ok ? nxt : -1;
             wp.pend_cur = pend_cur;
