@@ -40,7 +40,11 @@ namespace {
 #define EVOX_AHEAD 4  // mode-B prefetch window, in lane groups
 #endif
 #ifndef EVOX_PF
-#define EVOX_PF 3  // tuning: bit 0 enables mode-A (next rows), bit 1 mode-B (window) prefetch
+// L2 bulk-prefetch switches (measured): bit 0 mode A (a warp's next short
+// rows: +2-4 points at dim <= 1000), bit 1 mode B (sliding window inside long rows: -13
+// points at dim 1e5, off), bit 2 CSO winner/loser rows of the next item, bit 3 the first
+// rows of a PDL-launched generation.
+#define EVOX_PF 13
 #endif
 constexpr int U = EVOX_U;          // max chunks in flight per lane group (register slots)
 constexpr int WARPS = 8;           // warps per CTA (256 threads) in every geometry
@@ -158,7 +162,7 @@ template <class G>
 __device__ __forceinline__ void prefetch_first_rows(const float* X, const float* V, long long rows,
                                                     long long ld, long long wfirst, long long qb,
                                                     long long qe) {
-    if (lane_id() != 0 || wfirst >= rows) return;
+    if (!(EVOX_PF & 8) || lane_id() != 0 || wfirst >= rows) return;
     const long long nr = rows - wfirst < G::RPW ? rows - wfirst : G::RPW;
     const long long o = wfirst * ld * 4 + qb * 16;
     long long bytes = G::WPR == 1 ? nr * ld * 4 : (qe - qb) * 16;
@@ -1323,7 +1327,7 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_cso_gen(CsoArgs a) {
         const long long witem = m.wfirst + k * m.stride;
         if (witem >= items) break;
         const long long it = m.first + k * m.stride;
-        if (m.sl == 0 && ci_nxt.valid && ci_nxt.gl >= 0) {
+        if ((EVOX_PF & 4) && m.sl == 0 && ci_nxt.valid && ci_nxt.gl >= 0) {
             const char* X = reinterpret_cast<const char*>(a.X);
             const long long ol = (ci_nxt.gl - a.row0) * a.ld * 4 + seg_off;
             prefetch_l2(X + ol, seg_bytes);
