@@ -41,10 +41,10 @@ namespace {
 #endif
 #ifndef EVOX_PF
 // L2 bulk-prefetch switches (measured): bit 0 mode A (a warp's next short
-// rows: +2-4 points at dim <= 1000), bit 1 mode B (sliding window inside long rows: -13
-// points at dim 1e5, off), bit 2 CSO winner/loser rows of the next item, bit 3 the first
-// rows of a PDL-launched generation.
-#define EVOX_PF 13
+// rows: +2-4 points at dim <= 1000; on), bit 1 mode B (sliding window inside long rows:
+// -13 points at dim 1e5; off), bit 2 CSO winner/loser rows of the next item (neutral; off),
+// bit 3 the first rows of a PDL-launched generation (neutral; off).
+#define EVOX_PF 1
 #endif
 constexpr int U = EVOX_U;          // max chunks in flight per lane group (register slots)
 constexpr int WARPS = 8;           // warps per CTA (256 threads) in every geometry
