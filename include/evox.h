@@ -289,6 +289,10 @@ evox_status evox_de_history(evox_de* s, float* best_per_gen, int64_t cap, int64_
 evox_status evox_de_view(evox_de* s, int field, void** dev, int64_t* rows, int64_t* ld);
 evox_status evox_de_info(evox_de* s, int64_t* pop, int64_t* dim, int64_t* ld, int64_t* row0,
                          int64_t* rows, int64_t* t, void** cuda_stream);
+/* Checkpoint / resume of this rank's DE state (the population is gathered into
+ * one buffer first; same blob rules as evox_pso_save/load).  Synchronising. */
+evox_status evox_de_save(evox_de* s, void* host_blob, size_t cap, size_t* used);
+evox_status evox_de_load(evox_de* s, const void* host_blob, size_t size);
 evox_status evox_de_sync(evox_de* s);
 /* The state allocation of this rank: device base pointer and/or its 64-byte
  * cudaIpcMemHandle (NULL outputs are skipped). */

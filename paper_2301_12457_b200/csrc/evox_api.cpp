@@ -1673,6 +1673,75 @@ evox_status evox_de_step(evox_de* s, evox_problem problem, int64_t n_gens) {
     return EVOX_OK;
 }
 
+// Blob: header | X (gathered) | f (current parity) | hist[0..t]
+evox_status evox_de_save(evox_de* s, void* host_blob, size_t cap, size_t* used) {
+    evox_status st = check_de(s);
+    if (st != EVOX_OK) return st;
+    if (!used) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL used");
+    const size_t mat = sizeof(float) * (size_t)s->rows * (size_t)s->ld;
+    const int64_t T = s->t + 1;
+    const size_t need = sizeof(BlobHdr) + mat + 4 * (size_t)s->rows + 4 * (size_t)(T > 0 ? T : 0);
+    *used = need;
+    if (!host_blob) return EVOX_OK;
+    if (cap < need) return fail(EVOX_ERR_INVALID_ARGUMENT, "blob buffer too small");
+    DevGuard g(s->device);
+    CU(s, evox::launch_de_materialize(s->args(), s->stream));
+    st = sync_check(s);
+    if (st != EVOX_OK) return st;
+    const int p = (int)((s->t < 0 ? 0 : s->t) & 1);
+    BlobHdr h;
+    std::memset(&h, 0, sizeof h);
+    std::memcpy(h.magic, "EVOXDE01", 8);
+    h.kind = 2; h.pop = s->pop; h.dim = s->dim; h.ld = s->ld; h.row0 = s->row0; h.rows = s->rows;
+    h.t = s->t; h.problem = s->problem; h.world = s->world; h.rank = s->rank; h.seed = s->seed;
+    h.w = s->F; h.phi_p = s->CR;
+    char* q = static_cast<char*>(host_blob);
+    std::memcpy(q, &h, sizeof h);
+    q += sizeof h;
+    CU(s, cudaMemcpy(q, s->buf[0], mat, cudaMemcpyDeviceToHost)); q += mat;
+    CU(s, cudaMemcpy(q, s->f[p], 4 * s->rows, cudaMemcpyDeviceToHost)); q += 4 * s->rows;
+    if (T > 0) CU(s, cudaMemcpy(q, s->hist, 4 * T, cudaMemcpyDeviceToHost));
+    return EVOX_OK;
+}
+
+evox_status evox_de_load(evox_de* s, const void* host_blob, size_t size) {
+    evox_status st = check_de(s);
+    if (st != EVOX_OK) return st;
+    if (!host_blob || size < sizeof(BlobHdr)) return fail(EVOX_ERR_INVALID_ARGUMENT, "bad blob");
+    BlobHdr h;
+    std::memcpy(&h, host_blob, sizeof h);
+    if (std::memcmp(h.magic, "EVOXDE01", 8) != 0) return fail(EVOX_ERR_INVALID_ARGUMENT, "not a DE blob");
+    if (h.pop != s->pop || h.dim != s->dim || h.ld != s->ld || h.row0 != s->row0 ||
+        h.rows != s->rows || h.world != s->world || h.rank != s->rank)
+        return fail(EVOX_ERR_SHAPE, "blob shape/shard does not match the handle");
+    if (h.seed != s->seed || h.w != s->F || h.phi_p != s->CR)
+        return fail(EVOX_ERR_CONTRACT, "blob parameters (seed/F/CR) differ from the handle's");
+    const size_t mat = sizeof(float) * (size_t)s->rows * (size_t)s->ld;
+    const int64_t T = h.t + 1;
+    const size_t need = sizeof(BlobHdr) + mat + 4 * (size_t)s->rows + 4 * (size_t)(T > 0 ? T : 0);
+    if (size < need) return fail(EVOX_ERR_SHAPE, "blob truncated");
+    DevGuard g(s->device);
+    st = ensure_hist(s, (T > 0 ? T : 0) + 1);
+    if (st != EVOX_OK) return st;
+    CU(s, cudaStreamSynchronize(s->stream));
+    const int p = (int)((h.t < 0 ? 0 : h.t) & 1);
+    const char* q = static_cast<const char*>(host_blob) + sizeof h;
+    CU(s, cudaMemcpy(s->buf[0], q, mat, cudaMemcpyHostToDevice)); q += mat;
+    CU(s, cudaMemcpy(s->f[p], q, 4 * s->rows, cudaMemcpyHostToDevice)); q += 4 * s->rows;
+    if (T > 0) CU(s, cudaMemcpy(s->hist, q, 4 * T, cudaMemcpyHostToDevice));
+    CU(s, cudaMemset(s->sel[0], 0, s->rows));  // the population is in buf[0]
+    CU(s, cudaMemset(s->sel[1], 0, s->rows));
+    Ctl c;
+    CU(s, cudaMemcpy(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost));
+    c.gen_key = ~0ull;
+    c.ticket = 0;
+    c.t = h.t < 0 ? 0 : (unsigned long long)h.t;
+    CU(s, cudaMemcpy(s->ctl, &c, sizeof c, cudaMemcpyHostToDevice));
+    s->t = h.t;
+    s->problem = (int)h.problem;
+    return EVOX_OK;
+}
+
 evox_status evox_de_sync(evox_de* s) {
     evox_status st = check_de(s);
     if (st != EVOX_OK) return st;

@@ -114,6 +114,8 @@ SIGNATURES = {
     "evox_de_view": ([_p, _i, _PP, _PI64, _PI64], _i),
     "evox_de_info": ([_p, _PI64, _PI64, _PI64, _PI64, _PI64, _PI64, _PP], _i),
     "evox_de_sync": ([_p], _i),
+    "evox_de_save": ([_p, _p, ctypes.c_size_t, _PSZ], _i),
+    "evox_de_load": ([_p, _p, ctypes.c_size_t], _i),
     "evox_de_set_timing": ([_p, _i], _i),
     "evox_de_state": ([_p, _PP, _p], _i),
     "evox_de_connect": ([_p, _i, _p], _i),

@@ -174,3 +174,19 @@ def test_de_sharded_requires_connect():
     h = ev.DE(16, 4, -1, 1, rank=0, world=2)
     with pytest.raises(E.ContractError):
         h.step("sphere", 1)
+
+
+def test_de_save_load_roundtrip():
+    N, D, p = 40, 23, "rastrigin"
+    a = ev.DE(N, D, -5.12, 5.12, seed=4)
+    a.step(p, 6)
+    blob = a.save()
+    a.step(p, 5)
+    b = ev.DE(N, D, -5.12, 5.12, seed=4)
+    b.load(blob)
+    b.step(p, 5)
+    assert np.array_equal(_state(a, D)[0], _state(b, D)[0])
+    assert np.array_equal(a.history(), b.history())
+    c = ev.DE(N, D, -5.12, 5.12, seed=4, CR=0.5)
+    with pytest.raises(E.ContractError):
+        c.load(blob)
