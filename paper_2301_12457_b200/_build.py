@@ -20,8 +20,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", "-I", INCLUDE, "-I", CSRC,
           "-I", "/usr/include"]
-SOURCES = ["evox_kernels.cu", "evox_api.cpp", "nccl_dl.cpp"]
-HEADERS = ["evox_device.cuh", "evox_internal.h", "nccl_dl.h"]
+SOURCES = ["pso_kernels.cu", "cso_kernels.cu", "de_kernels.cu", "common_kernels.cu", "evox_api.cpp",
+           "nccl_dl.cpp"]
+HEADERS = ["evox_device.cuh", "row_engine.cuh", "evox_internal.h", "nccl_dl.h"]
 
 
 def _newest_input() -> float:

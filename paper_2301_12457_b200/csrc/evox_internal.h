@@ -117,9 +117,8 @@ struct DeArgs {
 
 // Launch configuration is a function of dim only (R-11: bitwise identical
 // results for every shard count and population size).
-int wpr_for_dim(long long ld);
 
-// ---- launchers (evox_kernels.cu); all asynchronous on `st`.
+// ---- launchers (pso/cso/de/common_kernels.cu); all asynchronous on `st`.
 cudaError_t launch_pso_init(const PsoArgs& a, cudaStream_t st);
 cudaError_t launch_eval(int problem, const float* X, long long rows, long long D, long long ld,
                         float* fit, cudaStream_t st);

@@ -1,0 +1,776 @@
+// pso_kernels.cu -- PSO: the fused generation kernel (A1-A12), its TMA-staged
+// variant, the persistent small-population kernel, the unfused ask/tell kernels and the
+// gbest exchange (A13: NCCL select or in-kernel peer-memory mailboxes).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "evox_device.cuh"
+#include "evox_internal.h"
+#include "row_engine.cuh"
+
+namespace evox {
+
+namespace {
+
+// PSO move of one row (A1, A3, A4, lazy A5).  Holds a reference to the kernel
+// parameter block (resolved to constant-bank operands once inlined: the
+// Philox round keys, w, phi*2^-24 and the bounds feed instructions directly).
+template <bool UNI, bool G_COHERENT = false>
+struct MoverPso {
+    const PsoArgs& a;
+    float4* Xr;
+    float4* Vr;
+    float4* Pr;
+    uint32_t row_g;  // global row (Philox counter word 1)
+    uint32_t t;      // generation of the source population (counter word 2)
+    bool pend;       // pbest copy pending: P := X_t, P not read
+    float4 x[U], v[U], p[U];
+    __device__ __forceinline__ MoverPso(const PsoArgs& a_, long long row, uint32_t t_, bool pend_)
+        : a(a_) {
+        Xr = reinterpret_cast<float4*>(a.X + row * a.ld);
+        Vr = reinterpret_cast<float4*>(a.V + row * a.ld);
+        Pr = reinterpret_cast<float4*>(a.P + row * a.ld);
+        row_g = (uint32_t)(a.row0 + row);
+        t = t_;
+        pend = pend_;
+    }
+    template <bool EF>
+    __device__ __forceinline__ void load(int u, long long q) {
+        x[u] = ld_stream<EF>(Xr + q);
+        v[u] = ld_stream<EF>(Vr + q);
+        if (!pend) p[u] = ld_stream<EF>(Pr + q);
+    }
+    __device__ __forceinline__ float4 step(int u, long long q) {
+        const float4 xo = x[u];
+        const float4 pb = pend ? xo : p[u];
+        if (pend) st_stream(Pr + q, xo);
+        // G is read-only for a generation kernel (non-coherent path); the
+        // persistent small-population kernel rewrites it between generations.
+        const float4 g = G_COHERENT ? __ldcg(reinterpret_cast<const float4*>(a.G) + q)
+                                    : __ldg(reinterpret_cast<const float4*>(a.G) + q);
+        const float4 lo = bound4t<UNI>(a.lb, a.lb0, q);
+        const float4 hi = bound4t<UNI>(a.ub, a.ub0, q);
+        const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 2u), a.rk);
+        const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 3u), a.rk);
+        float4 xn = xo, vn = v[u];
+        const float w = a.w, cp = a.cp, cg = a.cg;
+        pso_elem(xn.x, vn.x, pb.x, g.x, scaled_u24(b1.x, cp), scaled_u24(b2.x, cg), w, lo.x, hi.x);
+        pso_elem(xn.y, vn.y, pb.y, g.y, scaled_u24(b1.y, cp), scaled_u24(b2.y, cg), w, lo.y, hi.y);
+        pso_elem(xn.z, vn.z, pb.z, g.z, scaled_u24(b1.z, cp), scaled_u24(b2.z, cg), w, lo.z, hi.z);
+        pso_elem(xn.w, vn.w, pb.w, g.w, scaled_u24(b1.w, cp), scaled_u24(b2.w, cg), w, lo.w, hi.w);
+        zero_pad(xn, vn, q, a.D);
+        st_stream(Xr + q, xn);
+        st_stream(Vr + q, vn);
+        return xn;
+    }
+};
+
+// Mode-B prefetcher (long row segments): keeps a window of AHEAD quads of
+// X, V and (unless the pbest copy is pending) P in flight ahead of the
+// loads, crossing into the warp's next row.  Lane 0 issues; the cursor is
+// relative to the current row segment (c in [0, 2 seg)).
+struct WindowPrefetch {
+    const char* X;
+    const char* V;
+    const char* P;
+    long long ld_bytes, qb, seg, ahead;
+    long long row, nxt;  // current and next row of the warp (nxt >= rows: none)
+    bool pend_cur, pend_nxt, on;
+    long long c;         // next unprefetched quad, relative to qb of the current row
+    __device__ __forceinline__ void issue(long long r, long long q0, long long n, bool pend) {
+        const long long o = r * ld_bytes + (qb + q0) * 16;
+        prefetch_l2(X + o, n * 16);
+        prefetch_l2(V + o, n * 16);
+        if (!pend) prefetch_l2(P + o, n * 16);
+    }
+    __device__ __forceinline__ void operator()(long long base) {
+        if (!on) return;
+        long long target = (base - qb) + ahead;
+        const long long lim = nxt >= 0 ? 2 * seg : seg;
+        if (target > lim) target = lim;
+        if (c >= target) return;
+        if (c < seg) {
+            const long long e = target < seg ? target : seg;
+            issue(row, c, e - c, pend_cur);
+            c = e;
+        }
+        if (c < target) {  // into the next row
+            issue(nxt, c - seg, target - c, pend_nxt);
+            c = target;
+        }
+    }
+};
+
+// The last CTA's winner record -> every rank's mailbox slot[par][rank]; wait for
+// the world records of this generation; strict gbest selection (A13, fused).
+// Every rank selects from the same world records: identical G on all ranks.
+__device__ void peer_exchange(const PsoArgs& a, unsigned long long key, unsigned long long t_new) {
+    __shared__ int sh_w, sh_better;
+    __shared__ unsigned long long sh_key;
+    Ctl* ctl = a.ctl;
+    const long long NQ = a.ld >> 2;
+    const int par = (int)(t_new & 1);
+    const unsigned long long flag = t_new + 1;  // mailboxes start zeroed: 0 = nothing yet
+    const bool any = key != ~0ull;
+    const long long grow = (long long)(uint32_t)(key & 0xffffffffu);
+    const float4* src = reinterpret_cast<const float4*>(a.X + (any ? grow - a.row0 : 0) * a.ld);
+    const long long my_off = ((long long)par * a.world + a.rank) * a.mb_slot;
+    for (long long q = threadIdx.x; q < NQ; q += blockDim.x) {
+        const float4 v = any ? __ldcg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int p = 0; p < a.world; ++p)
+            reinterpret_cast<float4*>(a.mbox[p] + my_off + 16)[q] = v;
+    }
+    if (threadIdx.x == 0)
+        for (int p = 0; p < a.world; ++p)
+            *reinterpret_cast<unsigned long long*>(a.mbox[p] + my_off + 8) = key;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int p = 0; p < a.world; ++p)
+            st_release_sys(reinterpret_cast<unsigned long long*>(a.mbox[p] + my_off), flag);
+        // wait for every rank's record of this generation in our own mailbox
+        const unsigned long long t0 = globaltimer_ns();
+        unsigned long long kmin = ~0ull;
+        int w = -1;
+        for (int r = 0; r < a.world; ++r) {
+            const unsigned char* slot = a.mbox[a.rank] + ((long long)par * a.world + r) * a.mb_slot;
+            while (ld_acquire_sys(reinterpret_cast<const unsigned long long*>(slot)) != flag) {
+                if (globaltimer_ns() - t0 > a.peer_timeout_ns) {
+                    ctl->err = 1;
+                    break;
+                }
+                __nanosleep(256);
+            }
+            const unsigned long long kr = __ldcg(reinterpret_cast<const unsigned long long*>(slot + 8));
+            if (kr < kmin) { kmin = kr; w = r; }
+        }
+        const bool ok = kmin != ~0ull;
+        const float fmin = ok ? unord_f32((uint32_t)(kmin >> 32)) : __int_as_float(0x7f800000);
+        sh_key = kmin;
+        sh_w = w;
+        sh_better = ok && fmin < ctl->gf;  // strict improvement (R-5)
+    }
+    __syncthreads();
+    if (sh_better) {
+        const float4* wr = reinterpret_cast<const float4*>(
+            a.mbox[a.rank] + ((long long)par * a.world + sh_w) * a.mb_slot + 16);
+        float4* G = reinterpret_cast<float4*>(a.G);
+        for (long long q = threadIdx.x; q < NQ; q += blockDim.x) G[q] = __ldcg(wr + q);
+    }
+    if (threadIdx.x == 0) {
+        const unsigned long long k = sh_key;
+        const float fmin = k != ~0ull ? unord_f32((uint32_t)(k >> 32)) : __int_as_float(0x7f800000);
+        if (sh_better) {
+            ctl->gf = fmin;
+            ctl->gidx = (long long)(uint32_t)(k & 0xffffffffu);
+        }
+        ctl->hist[t_new] = fmin;
+    }
+}
+
+// In the last CTA: gbest update (strict, R-5), hist, or the winner record for
+// the exchange.  `t_new` is the index of the population just evaluated.
+__device__ void pso_finalize(const PsoArgs& a, unsigned long long key, unsigned long long t_new) {
+    Ctl* ctl = a.ctl;
+    const long long NQ = a.ld >> 2;
+    const bool any = key != ~0ull;
+    const long long grow = (long long)(uint32_t)(key & 0xffffffffu);
+    const float fmin = any ? unord_f32((uint32_t)(key >> 32)) : __int_as_float(0x7f800000);
+    if (a.peer) {
+        peer_exchange(a, key, t_new);
+    } else if (a.exchange) {
+        // winner record {u64 key; u32 pad[2]; f32 row[ld]} into this rank's slot
+        unsigned char* rec = a.rec + (long long)a.rank * a.rec_stride;
+        const float4* src = reinterpret_cast<const float4*>(a.X + (any ? grow - a.row0 : 0) * a.ld);
+        float4* dst = reinterpret_cast<float4*>(rec + 16);
+        for (long long q = threadIdx.x; q < NQ; q += blockDim.x)
+            dst[q] = any ? __ldcg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (threadIdx.x == 0) *reinterpret_cast<unsigned long long*>(rec) = key;
+    } else {
+        __shared__ int sh_better;
+        if (threadIdx.x == 0) sh_better = any && fmin < ctl->gf;  // strict improvement
+        __syncthreads();
+        const bool better = sh_better != 0;
+        if (better) {
+            const float4* src = reinterpret_cast<const float4*>(a.X + (grow - a.row0) * a.ld);
+            float4* G = reinterpret_cast<float4*>(a.G);
+            for (long long q = threadIdx.x; q < NQ; q += blockDim.x) G[q] = __ldcg(src + q);
+        }
+        if (threadIdx.x == 0) {
+            if (better) {
+                ctl->gf = fmin;
+                ctl->gidx = grow;
+            }
+            ctl->hist[t_new] = fmin;
+        }
+    }
+    if (threadIdx.x == 0) {
+        ctl->gen_key = ~0ull;
+        ctl->ticket = 0u;
+        ctl->t = t_new;
+    }
+}
+
+__global__ void k_pso_init(PsoArgs a) {
+    init_population(a.X, a.V, a.P, a.rows, a.row0, a.D, a.ld, a.lb, a.ub, a.lb0, a.ub0,
+                    a.uniform_bounds, a.rk);
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < a.rows;
+         r += (long long)gridDim.x * blockDim.x) {
+        a.pf[r] = __int_as_float(0x7f800000);
+        a.f[r] = __int_as_float(0x7f800000);
+        a.imp[r] = 0;
+    }
+}
+
+// Fused PSO generation: lazy pbest + move + clip + evaluate + tell + argmin.
+template <int P, class G, bool UNI>
+__global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen(PsoArgs a) {
+    __shared__ Fit<P> sh_acc[G::WPR];
+    __shared__ float sh_head[G::WPR];
+    __shared__ __align__(16) HStore<P> sh_h;
+    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+    const RowMap<G> m(a.ld >> 2);
+    const int lane = lane_id();
+    prefetch_first_rows<G>(a.X, a.V, a.rows, a.ld, m.wfirst, m.qb, m.qe);
+    pdl_wait();               // the previous generation (G, imp, pf, t) is complete
+    pdl_launch_dependents();  // the next generation may be scheduled as our CTAs retire
+    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
+    const long long seg = m.qe - m.qb;
+    // prefetch mode: A = the warp's whole next rows (short rows), B = sliding window
+    const bool mode_a = seg * G::RPW <= MODE_A_MAX;
+    WindowPrefetch wp;
+    wp.X = reinterpret_cast<const char*>(a.X);
+    wp.V = reinterpret_cast<const char*>(a.V);
+    wp.P = reinterpret_cast<const char*>(a.P);
+    wp.ld_bytes = a.ld * 4;
+    wp.qb = m.qb;
+    wp.seg = seg;
+    wp.ahead = seg < EVOX_AHEAD * G::GROUP ? seg : EVOX_AHEAD * G::GROUP;
+    wp.on = !mode_a && lane == 0 && (EVOX_PF & 2);
+    wp.c = 0;
+    unsigned long long best = ~0ull;
+    // pbest-pending flags one and two iterations ahead (imp[r] is rewritten only
+    // by the thread group that owns row r, later in this kernel, so these reads
+    // see the previous generation's decisions).
+    long long row = m.first;
+    bool pend_cur = row < a.rows ? a.imp[row] != 0 : true;
+    bool pend_nxt = row + m.stride < a.rows ? a.imp[row + m.stride] != 0 : true;
+    for (long long it = 0;; ++it, row += m.stride) {
+        const long long wrow = m.wfirst + it * m.stride;
+        if (wrow >= a.rows) break;  // warp-uniform (CTA-uniform for WPR > 1)
+        const bool ok = row < a.rows;
+        const long long nxt = row + m.stride, nn = nxt + m.stride;
+        const bool nxt_ok = nxt < a.rows;
+        if (mode_a && (EVOX_PF & 1)) {
+            // the warp's next rows, HBM -> L2 now (X, V contiguous; P per row unless pending)
+            const long long wn = wrow + m.stride;
+            if (lane == 0 && wn < a.rows) {
+                long long nr = a.rows - wn < G::RPW ? a.rows - wn : G::RPW;
+                const long long o = wn * a.ld * 4 + m.qb * 16;
+                const long long bytes = G::WPR == 1 ? nr * a.ld * 4 : seg * 16;
+                prefetch_l2(reinterpret_cast<const char*>(a.X) + o, bytes);
+                prefetch_l2(reinterpret_cast<const char*>(a.V) + o, bytes);
+            }
+            if (m.sl == 0 && nxt_ok && !pend_nxt)
+                prefetch_l2(reinterpret_cast<const char*>(a.P) + nxt * a.ld * 4 + m.qb * 16,
+                            seg * 16);
+        } else if (!mode_a) {
+            wp.row = row;
+            wp.nxt = nxt_ok ? nxt : -1;
+            wp.pend_cur = pend_cur;
+            wp.pend_nxt = pend_nxt;
+        }
+        const bool pend_nn = nn < a.rows ? a.imp[nn] != 0 : true;
+        float pf_old = 0.0f;
+        if (m.leader && ok) pf_old = a.pf[row];
+        MoverPso<UNI> mv(a, ok ? row : 0, (uint32_t)t, pend_cur);
+        Fit<P> acc;
+        float hx, tx;
+        bool tv;
+        walk_segment<P, G>(mv, m.qb, m.qe, a.D, ok, acc, hx, tx, tv, wp, htab);
+        const float f = reduce_row<P, G>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
+        if (m.leader && ok) {
+            // per-row tell (A11): strict improvement, NaN never improves
+            const bool imp = f < pf_old;
+            a.f[row] = f;
+            a.imp[row] = imp ? 1 : 0;
+            if (imp) a.pf[row] = f;
+            const unsigned long long k = make_key(f, a.row0 + row);
+            best = k < best ? k : best;
+        }
+        pend_cur = pend_nxt;
+        pend_nxt = pend_nn;
+        wp.c = wp.c > seg ? wp.c - seg : 0;
+    }
+    unsigned long long key;
+    if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
+}
+
+
+// Persistent single-CTA PSO for tiny populations (latency-bound, e.g. C1:
+// 100 x 10): all n generations in one launch, a CTA barrier instead of the
+// grid-wide argmin.  Per-row arithmetic, reduction order and decisions are
+// those of k_pso_gen, so the trajectory is bitwise identical.
+template <int P, class G, bool UNI>
+__global__ void __launch_bounds__(256) k_pso_run_small(PsoArgs a, long long n_gens) {
+    __shared__ Fit<P> sh_acc[G::WPR];
+    __shared__ float sh_head[G::WPR];
+    __shared__ __align__(16) HStore<P> sh_h;
+    __shared__ unsigned long long sh_k[WARPS];
+    __shared__ int sh_better;
+    __shared__ long long sh_row;
+    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+    const RowMap<G> m(a.ld >> 2);
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    Ctl* ctl = a.ctl;
+    unsigned long long t = ctl->t;
+    float gf = ctl->gf;
+    long long gidx = ctl->gidx;
+    NoPrefetch pf;
+    for (long long g = 0; g < n_gens; ++g) {
+        unsigned long long best = ~0ull;
+        for (long long it = 0;; ++it) {
+            const long long wrow = m.wfirst + it * m.stride;
+            if (wrow >= a.rows) break;
+            const long long row = m.first + it * m.stride;
+            const bool ok = row < a.rows;
+            const bool pend = ok ? a.imp[row] != 0 : true;
+            float pf_old = 0.0f;
+            if (m.leader && ok) pf_old = a.pf[row];
+            MoverPso<UNI, true> mv(a, ok ? row : 0, (uint32_t)t, pend);
+            Fit<P> acc;
+            float hx, tx;
+            bool tv;
+            walk_segment<P, G>(mv, m.qb, m.qe, a.D, ok, acc, hx, tx, tv, pf, htab);
+            const float f = reduce_row<P, G>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
+            if (m.leader && ok) {
+                const bool imp = f < pf_old;
+                a.f[row] = f;
+                a.imp[row] = imp ? 1 : 0;
+                if (imp) a.pf[row] = f;
+                const unsigned long long k = make_key(f, a.row0 + row);
+                best = k < best ? k : best;
+            }
+        }
+        best = warp_min_u64(best);
+        if (lane == 0) sh_k[wid] = best;
+        __syncthreads();  // also orders this generation's X stores before the G copy
+        if (threadIdx.x == 0) {
+            unsigned long long k = sh_k[0];
+            for (int i = 1; i < WARPS; ++i) k = sh_k[i] < k ? sh_k[i] : k;
+            const bool any = k != ~0ull;
+            const float fmin = any ? unord_f32((uint32_t)(k >> 32)) : __int_as_float(0x7f800000);
+            const bool better = any && fmin < gf;  // strict improvement
+            sh_better = better;
+            sh_row = (long long)(uint32_t)(k & 0xffffffffu) - a.row0;
+            if (better) {
+                gf = fmin;
+                gidx = (long long)(uint32_t)(k & 0xffffffffu);
+            }
+            ctl->hist[t + 1] = fmin;
+        }
+        __syncthreads();
+        if (sh_better) {
+            const float4* src = reinterpret_cast<const float4*>(a.X + sh_row * a.ld);
+            float4* Gd = reinterpret_cast<float4*>(a.G);
+            for (long long q = threadIdx.x; q < (a.ld >> 2); q += blockDim.x) Gd[q] = __ldcg(src + q);
+        }
+        __syncthreads();
+        ++t;
+    }
+    if (threadIdx.x == 0) {
+        ctl->t = t;
+        ctl->gf = gf;
+        ctl->gidx = gidx;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged fused PSO generation (warp-per-row geometry, ld <= 4096).
+// Each warp owns a 2-stage shared-memory ring of {X, V, P} x 128 quads (one
+// lane group).  Lane 0 fills it with cp.async.bulk (1-D TMA, SASS UBLKCP)
+// completing on a per-stage mbarrier: while the warp computes group g from
+// shared memory, group g+1 (possibly the first group of the warp's next row)
+// is in flight -- no registers held by in-flight loads, and the 4 chunks of a
+// group are still computed straight-line (cross-chunk Philox ILP).  Stores go
+// straight from registers (evict-first).  Same arithmetic, reduction tree and
+// decisions as k_pso_gen: bitwise identical (tested).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+constexpr int TMA_GQ = 32 * U;  // quads per group (= G32::GROUP)
+struct TmaStage {
+    float4 x[TMA_GQ], v[TMA_GQ], p[TMA_GQ];
+};
+constexpr size_t TMA_SMEM = sizeof(TmaStage) * 2 * WARPS;  // 96 KB per CTA
+
+template <int P, bool UNI>
+__global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen_tma(PsoArgs a) {
+    using G = Geom<32, 1>;  // the warp-per-row geometry (G32)
+    extern __shared__ __align__(128) unsigned char dyn_smem[];
+    __shared__ __align__(8) uint64_t bars[WARPS][2];
+    __shared__ Fit<P> sh_acc[1];
+    __shared__ float sh_head[1];
+    __shared__ __align__(16) HStore<P> sh_h;
+    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+    const RowMap<G> m(a.ld >> 2);
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    TmaStage* stg = reinterpret_cast<TmaStage*>(dyn_smem) + 2 * wid;
+    uint64_t* bar = bars[wid];
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    pdl_wait();
+    pdl_launch_dependents();
+    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
+    const long long NQ = a.ld >> 2;
+    const long long NG = (NQ + TMA_GQ - 1) / TMA_GQ;  // groups per row
+    const long long n_it = m.wfirst < a.rows ? (a.rows - 1 - m.wfirst) / m.stride + 1 : 0;
+    const long long total = n_it * NG;
+    const float4* X4 = reinterpret_cast<const float4*>(a.X);
+    const float4* V4 = reinterpret_cast<const float4*>(a.V);
+    const float4* P4 = reinterpret_cast<const float4*>(a.P);
+    // pbest-pending flags of the current row and the next two rows of the warp
+    long long row = m.first;
+    bool pend[3];
+    pend[0] = row < a.rows ? a.imp[row] != 0 : true;
+    pend[1] = row + m.stride < a.rows ? a.imp[row + m.stride] != 0 : true;
+    pend[2] = row + 2 * m.stride < a.rows ? a.imp[row + 2 * m.stride] != 0 : true;
+    // lane 0: put group g of the warp's stream in flight (it_cur = current row iteration)
+    auto issue = [&](long long g, long long it_cur) {
+        const long long it = g / NG, gg = g - it * NG;
+        const long long r = m.first + it * m.stride;
+        const long long q0 = gg * TMA_GQ;
+        const long long nq = NQ - q0 < TMA_GQ ? NQ - q0 : TMA_GQ;
+        const int st = (int)(g & 1);
+        const long long d = it - it_cur;
+        const bool pd = d == 0 ? pend[0] : (d == 1 ? pend[1] : pend[2]);
+        const uint32_t bytes = (uint32_t)(nq * 16);
+        fence_proxy_async_smem();  // the warp's generic reads of this stage are done
+        mbar_expect_tx(&bar[st], bytes * (pd ? 2u : 3u));
+        const long long o = r * NQ + q0;
+        tma_load_1d(stg[st].x, X4 + o, bytes, &bar[st]);
+        tma_load_1d(stg[st].v, V4 + o, bytes, &bar[st]);
+        if (!pd) tma_load_1d(stg[st].p, P4 + o, bytes, &bar[st]);
+    };
+    if (lane == 0 && total > 0) issue(0, 0);
+    float pf_old = 0.0f;
+    if (lane == 0 && row < a.rows) pf_old = a.pf[row];
+    Fit<P> acc;
+    float pend_x = 0.0f, head_x = 0.0f;
+    bool hpend = false;
+    unsigned long long best = ~0ull;
+    const float w = a.w, cp = a.cp, cg = a.cg;
+    long long it = 0, gg = 0;
+    for (long long g = 0; g < total; ++g) {
+        if (lane == 0 && g + 1 < total) issue(g + 1, it);  // stage (g+1)&1 was freed by g-1
+        const int st = (int)(g & 1);
+        mbar_wait(&bar[st], (uint32_t)((g >> 1) & 1));
+        const bool ok = row < a.rows;
+        const bool pd = pend[0];
+        const long long q0 = gg * TMA_GQ;
+        const uint32_t row_g = (uint32_t)(a.row0 + row);
+        float4* Xr = reinterpret_cast<float4*>(a.X) + row * NQ;
+        float4* Vr = reinterpret_cast<float4*>(a.V) + row * NQ;
+        float4* Pr = reinterpret_cast<float4*>(a.P) + row * NQ;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long cb = q0 + 32 * u;
+            if (cb >= NQ) break;  // warp-uniform
+            const long long q = cb + lane;
+            const bool valid = ok && q < NQ;
+            float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid) {
+                const int k = 32 * u + lane;
+                const float4 xo = stg[st].x[k];
+                float4 vn = stg[st].v[k];
+                const float4 pb = pd ? xo : stg[st].p[k];
+                if (pd) st_stream(Pr + q, xo);
+                const float4 g4 = __ldg(reinterpret_cast<const float4*>(a.G) + q);
+                const float4 lo = bound4t<UNI>(a.lb, a.lb0, q);
+                const float4 hi = bound4t<UNI>(a.ub, a.ub0, q);
+                const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, (uint32_t)t, 2u), a.rk);
+                const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, (uint32_t)t, 3u), a.rk);
+                xn = xo;
+                pso_elem(xn.x, vn.x, pb.x, g4.x, scaled_u24(b1.x, cp), scaled_u24(b2.x, cg), w, lo.x, hi.x);
+                pso_elem(xn.y, vn.y, pb.y, g4.y, scaled_u24(b1.y, cp), scaled_u24(b2.y, cg), w, lo.y, hi.y);
+                pso_elem(xn.z, vn.z, pb.z, g4.z, scaled_u24(b1.z, cp), scaled_u24(b2.z, cg), w, lo.z, hi.z);
+                pso_elem(xn.w, vn.w, pb.w, g4.w, scaled_u24(b1.w, cp), scaled_u24(b2.w, cg), w, lo.w, hi.w);
+                zero_pad(xn, vn, q, a.D);
+                st_stream(Xr + q, xn);
+                st_stream(Vr + q, vn);
+                fit_quad<P>(acc, xn, 4 * q, a.D, htab);
+            }
+            if constexpr (P == ROSENBROCK) {
+                const float nb = __shfl_down_sync(FULL, xn.x, 1);
+                const float f0 = __shfl_sync(FULL, xn.x, 0);
+                if (cb == 0) head_x = f0;
+                if (lane == 31 && hpend) {
+                    acc.pair(pend_x, f0);
+                    hpend = false;
+                }
+                if (valid && q + 1 < NQ) {
+                    const bool has_next = 4 * q + 4 < a.D;
+                    if (lane < 31) {
+                        if (has_next) acc.pair(xn.w, nb);
+                    } else {
+                        hpend = has_next;
+                        pend_x = xn.w;
+                    }
+                }
+            }
+        }
+        __syncwarp();  // all lanes are done reading stage st (reused by group g+2)
+        if (gg == NG - 1) {  // end of the row
+            const float f = reduce_row<P, G>(acc, a.D, head_x, 0.0f, false, sh_acc, sh_head);
+            if (lane == 0 && ok) {
+                const bool imp = f < pf_old;  // per-row tell (A11)
+                a.f[row] = f;
+                a.imp[row] = imp ? 1 : 0;
+                if (imp) a.pf[row] = f;
+                const unsigned long long k = make_key(f, a.row0 + row);
+                best = k < best ? k : best;
+            }
+            acc = Fit<P>();
+            hpend = false;
+            pend_x = head_x = 0.0f;
+            ++it;
+            gg = 0;
+            row += m.stride;
+            pend[0] = pend[1];
+            pend[1] = pend[2];
+            const long long r2 = row + 2 * m.stride;
+            pend[2] = r2 < a.rows ? a.imp[r2] != 0 : true;
+            if (lane == 0 && row < a.rows) pf_old = a.pf[row];
+        } else {
+            ++gg;
+        }
+    }
+    unsigned long long key;
+    if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
+}
+
+// Unfused ask: move X_t -> X_{t+1} (no evaluation).
+template <class G, bool UNI>
+__global__ void __launch_bounds__(256) k_pso_move(PsoArgs a, unsigned long long t) {
+    __shared__ Fit<SPHERE> sh_acc[G::WPR];
+    __shared__ float sh_head[G::WPR];
+    (void)sh_acc;
+    (void)sh_head;
+    const RowMap<G> m(a.ld >> 2);
+    NoPrefetch pf;
+    for (long long it = 0;; ++it) {
+        const long long wrow = m.wfirst + it * m.stride;
+        if (wrow >= a.rows) break;
+        const long long row = m.first + it * m.stride;
+        const bool ok = row < a.rows;
+        const bool pend = ok ? a.imp[row] != 0 : false;
+        MoverPso<UNI> mv(a, ok ? row : 0, (uint32_t)t, pend);
+        Fit<SPHERE> acc;  // unused
+        float hx, tx;
+        bool tv;
+        walk_segment<SPHERE, G>(mv, m.qb, m.qe, a.D, ok, acc, hx, tx, tv, pf);
+        __syncwarp();
+        if constexpr (G::WPR > 1) __syncthreads();
+        if (m.leader && ok) a.imp[row] = 0;
+    }
+}
+
+// Tell with given fitness (t = 0 after init, or after an unfused ask).
+__global__ void __launch_bounds__(256) k_pso_tell(PsoArgs a, const float* __restrict__ fit,
+                                                  unsigned long long t) {
+    unsigned long long best = ~0ull;
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < a.rows;
+         r += (long long)gridDim.x * blockDim.x) {
+        const float f = fit[r];
+        const bool imp = f < a.pf[r];
+        a.f[r] = f;
+        a.imp[r] = imp ? 1 : 0;
+        if (imp) a.pf[r] = f;
+        const unsigned long long k = make_key(f, a.row0 + r);
+        best = k < best ? k : best;
+    }
+    unsigned long long key;
+    if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t);
+}
+
+// world > 1: after the all-gather of the W winner records, pick the min key
+// (fitness, then global index) and apply the strict gbest improvement (A13).
+__global__ void __launch_bounds__(256) k_gbest_select(PsoArgs a) {
+    __shared__ int sh_w;
+    __shared__ unsigned long long sh_key;
+    Ctl* ctl = a.ctl;
+    if (threadIdx.x == 0) {
+        unsigned long long k = ~0ull;
+        int w = -1;
+        for (int r = 0; r < a.world; ++r) {
+            const unsigned long long kr =
+                *reinterpret_cast<const unsigned long long*>(a.rec + (long long)r * a.rec_stride);
+            if (kr < k) { k = kr; w = r; }
+        }
+        sh_w = w;
+        sh_key = k;
+    }
+    __syncthreads();
+    const unsigned long long key = sh_key;
+    const bool any = key != ~0ull;
+    const float fmin = any ? unord_f32((uint32_t)(key >> 32)) : __int_as_float(0x7f800000);
+    const bool better = any && fmin < ctl->gf;
+    if (better) {
+        const float4* src =
+            reinterpret_cast<const float4*>(a.rec + (long long)sh_w * a.rec_stride + 16);
+        float4* G = reinterpret_cast<float4*>(a.G);
+        for (long long q = threadIdx.x; q < (a.ld >> 2); q += blockDim.x) G[q] = src[q];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (better) {
+            ctl->gf = fmin;
+            ctl->gidx = (long long)(uint32_t)(key & 0xffffffffu);
+        }
+        ctl->hist[ctl->t] = fmin;
+    }
+}
+
+// Materialise pending pbest rows: P_i <- X_i, imp_i <- 0 (bitwise-neutral).
+__global__ void __launch_bounds__(256) k_pso_materialize(PsoArgs a) {
+    const long long NQ = a.ld >> 2;
+    const int wid = threadIdx.x >> 5, lane = lane_id();
+    for (long long row = (long long)blockIdx.x * WARPS + wid; row < a.rows;
+         row += (long long)gridDim.x * WARPS) {
+        if (!a.imp[row]) continue;
+        const float4* x = reinterpret_cast<const float4*>(a.X + row * a.ld);
+        float4* p = reinterpret_cast<float4*>(a.P + row * a.ld);
+        for (long long q = lane; q < NQ; q += 32) p[q] = x[q];
+        __syncwarp();
+        if (lane == 0) a.imp[row] = 0;
+    }
+}
+
+
+}  // namespace
+
+cudaError_t launch_pso_init(const PsoArgs& a, cudaStream_t st) {
+    const long long total = a.rows * (a.ld >> 2);
+    long long g = (total + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+    k_pso_init<<<(int)g, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+int pso_gen_grid(int problem, long long ld, long long rows, int device) {
+    int g = 1;
+    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
+        g = grid_for((const void*)k_pso_gen<P_, G_, true>, row_units<G_>(rows), device);
+    }));
+    return g;  // the TMA variant uses the same grid (2 CTAs/SM: 2 x 96 KB of staging)
+}
+
+// The TMA-staged kernel is an opt-in variant (EVOX_TMA=1) of the warp-per-row
+// geometry: measured 4-5 points BELOW the LDG + bulk-L2-prefetch kernel at H
+// and C2, so the LDG kernel is the default.
+static bool use_tma(long long ld) {
+    const char* v = getenv("EVOX_TMA");
+    return geom_id(ld) == 1 && U == 4 && v && *v == '1';
+}
+
+template <class K>
+static void tma_attr(K kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
+}
+
+cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
+    if (use_tma(a.ld)) {
+        EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, {
+            tma_attr(k_pso_gen_tma<P_, U_>);
+            e = launch_pdl(k_pso_gen_tma<P_, U_>, grid, a, st, TMA_SMEM);
+        }));
+    } else {
+        EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+            e = launch_pdl(k_pso_gen<P_, G_, U_>, grid, a, st);
+        })));
+    }
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+bool pso_small(long long rows, long long ld) { return rows * ld <= 65536; }
+
+cudaError_t launch_pso_run_small(int problem, const PsoArgs& a, long long n, cudaStream_t st) {
+    EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+        k_pso_run_small<P_, G_, U_><<<1, 256, 0, st>>>(a, n);
+    })));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pso_move(const PsoArgs& a, unsigned long long t, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_GEOM(a.ld, {
+        const int g = grid_for((const void*)k_pso_move<G_, U_>, row_units<G_>(a.rows), dev);
+        k_pso_move<G_, U_><<<g, 256, 0, st>>>(a, t);
+    }));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pso_tell(const PsoArgs& a, const float* fit, unsigned long long t,
+                            cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int g = grid_for((const void*)k_pso_tell, (a.rows + 255) / 256, dev);
+    k_pso_tell<<<g, 256, 0, st>>>(a, fit, t);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gbest_select(const PsoArgs& a, cudaStream_t st) {
+    k_gbest_select<<<1, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pso_materialize(const PsoArgs& a, cudaStream_t st) {
+    long long g = (a.rows + WARPS - 1) / WARPS;
+    if (g > 148 * 8) g = 148 * 8;
+    if (g < 1) g = 1;
+    k_pso_materialize<<<(int)g, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+
+}  // namespace evox
