@@ -234,8 +234,11 @@ evox_status evox_pso_destroy(evox_pso* s);
  * (evox_cso_state / evox_cso_connect, as for DE): each rank updates the losers
  * it owns, reading partner fitness and winner rows through peer memory, with
  * an in-kernel barrier + global minimum per generation.
- * phi: social factor of the mean-position term (0 by default; phi != 0 is
- * supported only for world == 1 in this version -> EVOX_ERR_CONFIG). */
+ * phi: social factor of the mean-position term (0 by default).  phi != 0 adds
+ * a per-generation column mean x-bar of the whole population (R-15: exact
+ * fixed-point sums; with world > 1 the ranks' sums are combined through peer
+ * memory when connected, else with one NCCL all-reduce -- bitwise the same
+ * trajectory for every world size). */
 evox_status evox_cso_workspace_bytes(int64_t pop, int64_t dim, int world, int rank, size_t* bytes);
 evox_status evox_cso_init(int64_t pop, int64_t dim, const float* lb, const float* ub, float phi,
                           int64_t block, uint64_t seed, const evox_opts* opts, evox_cso** out);

@@ -283,25 +283,82 @@ __global__ void k_cso_init(CsoArgs a) {
                     a.uniform_bounds, a.rk);
 }
 
-// Column means for the phi != 0 term: fixed row chunks of 1024, fp64 partial
-// sums in row order, chunks combined in order (world == 1 only).
-__global__ void k_colsum_partial(const float* __restrict__ X, long long rows, long long ld,
-                                 double* __restrict__ part) {
-    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long c = blockIdx.y;
-    if (j >= ld) return;
-    const long long r0 = c * 1024, r1 = (r0 + 1024 < rows) ? r0 + 1024 : rows;
-    double s = 0.0;
-    for (long long r = r0; r < r1; ++r) s += (double)X[r * ld + j];
-    part[c * ld + j] = s;
+// Column means for the phi != 0 term (R-15).  x is quantised to the fixed-point
+// grid 2^-qs (qs = 54 - ceil(log2 max|bound|), so |q| <= 2^54) and summed as exact
+// integers: int64 per 256-row chunk (|sum| < 2^62), folded into two carry-free
+// 64-bit limbs (the chunk sum's low 32 bits, unsigned, and its high part,
+// signed).  Integer addition is associative, so every partition of the rows --
+// CTAs, shards, NCCL or peer reduction order -- gives the same limbs and hence a
+// bitwise identical x-bar for every world size.
+constexpr long long COL_CH = 256;
+__global__ void k_colsum(const float* __restrict__ X, long long rows, long long ld, double scale,
+                         unsigned long long* __restrict__ limb) {
+    const long long NQ = ld >> 2;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= NQ) return;
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    const long long nch = (rows + COL_CH - 1) / COL_CH;
+    for (long long c = blockIdx.y; c < nch; c += gridDim.y) {
+        const long long r0 = c * COL_CH, r1 = r0 + COL_CH < rows ? r0 + COL_CH : rows;
+        long long cs[4] = {0, 0, 0, 0};
+#pragma unroll 4
+        for (long long r = r0; r < r1; ++r) {
+            const float4 x = __ldcs(X4 + r * NQ + q);
+            cs[0] += __double2ll_rn((double)x.x * scale);
+            cs[1] += __double2ll_rn((double)x.y * scale);
+            cs[2] += __double2ll_rn((double)x.z * scale);
+            cs[3] += __double2ll_rn((double)x.w * scale);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            atomicAdd(&limb[4 * q + k], (unsigned long long)cs[k] & 0xffffffffull);
+            atomicAdd(&limb[ld + 4 * q + k], (unsigned long long)(cs[k] >> 32));
+        }
+    }
 }
-__global__ void k_colsum_final(const double* __restrict__ part, long long nchunk, long long rows,
-                               long long ld, float* __restrict__ xbar) {
+
+// x-bar[j] = (sum_w limbs_w[j]) 2^-qs / pop.  With peers (evox_cso_connect) every
+// CTA first publishes "my limbs are final for generation t" into every rank's
+// flag slot and waits for all W flags (st.release.sys / ld.acquire.sys); the
+// limbs are single-buffered because no rank zeroes them for t+1 before the
+// end-of-generation barrier of t.  Without peers the limbs are already global
+// (W = 1, or NCCL-summed).
+__global__ void k_colmean(CsoArgs a, double inv_scale) {
+    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
+    if (a.peer) {
+        __shared__ int ok;
+        if (threadIdx.x == 0) {
+            const unsigned long long flag = t + 1;
+            __threadfence_system();
+            for (int w = 0; w < a.world; ++w) st_release_sys(a.pcflag[w] + a.rank, flag);
+            const unsigned long long t0 = globaltimer_ns();
+            ok = 1;
+            for (int w = 0; w < a.world && ok; ++w) {
+                while (ld_acquire_sys(a.pcflag[a.rank] + w) < flag) {
+                    if (globaltimer_ns() - t0 > a.peer_timeout_ns) {
+                        a.ctl->err = 1;
+                        ok = 0;
+                        break;
+                    }
+                    __nanosleep(128);
+                }
+            }
+        }
+        __syncthreads();
+        if (!ok) return;
+    }
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= ld) return;
-    double s = 0.0;
-    for (long long c = 0; c < nchunk; ++c) s += part[c * ld + j];
-    xbar[j] = (float)(s / (double)rows);
+    if (j >= a.ld) return;
+    unsigned long long lo = 0, hi = 0;
+    const int n = a.peer ? a.world : 1;
+    for (int w = 0; w < n; ++w) {
+        const unsigned long long* l = a.peer ? a.plimb[w] : a.limb;
+        lo += __ldcg(l + j);
+        hi += __ldcg(l + a.ld + j);
+    }
+    const long long h = (long long)hi + (long long)(lo >> 32);  // S = h 2^32 + (lo mod 2^32)
+    const double S = __fma_rn((double)h, 4294967296.0, (double)(lo & 0xffffffffull));
+    a.xbar[j] = (float)(S * inv_scale / (double)a.pop);
 }
 
 // world > 1: hist[t] from the all-reduced (min) keys.
@@ -354,12 +411,15 @@ cudaError_t launch_cso_gen(int problem, const CsoArgs& a, int grid, cudaStream_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_cso_colmean(const CsoArgs& a, float* xbar, double* scratch, cudaStream_t st) {
-    const long long nchunk = (a.rows + 1023) / 1024;
-    dim3 g1((unsigned)((a.ld + 127) / 128), (unsigned)nchunk);
-    k_colsum_partial<<<g1, 128, 0, st>>>(a.X, a.rows, a.ld, scratch);
-    k_colsum_final<<<(unsigned)((a.ld + 127) / 128), 128, 0, st>>>(scratch, nchunk, a.rows, a.ld,
-                                                                    xbar);
+cudaError_t launch_cso_colsum(const CsoArgs& a, double scale, cudaStream_t st) {
+    const long long NQ = a.ld >> 2, nch = (a.rows + COL_CH - 1) / COL_CH;
+    dim3 g((unsigned)((NQ + 127) / 128), (unsigned)(nch < 65535 ? nch : 65535));
+    k_colsum<<<g, 128, 0, st>>>(a.X, a.rows, a.ld, scale, a.limb);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cso_colmean(const CsoArgs& a, double inv_scale, cudaStream_t st) {
+    k_colmean<<<(unsigned)((a.ld + 255) / 256), 256, 0, st>>>(a, inv_scale);
     return cudaGetLastError();
 }
 

@@ -1014,7 +1014,15 @@ struct evox_cso : Base {
     float *X = nullptr, *V = nullptr, *xbar = nullptr;
     float* f2[2] = {nullptr, nullptr};  // fitness by generation parity
     float* fcur() const { return f2[(t < 0 ? 0 : t) & 1]; }
-    double* colpart = nullptr;
+    // phi != 0 (R-15): fixed-point column-sum limbs, their scale 2^qs, and every
+    // rank's limbs / column-sum flags when connected
+    unsigned long long* limb = nullptr;
+    double qscale = 1.0, qinv = 1.0;
+    unsigned long long* plimb[evox::kMaxPeers] = {};
+    unsigned long long* pcflag[evox::kMaxPeers] = {};
+    unsigned long long* cflag() const {
+        return reinterpret_cast<unsigned long long*>(mbox + (size_t)32 * (world > 1 ? world : 1));
+    }
     unsigned long long* keybuf = nullptr;
     int gen_grid[5] = {0, 0, 0, 0, 0};
     CsoArgs args() const {
@@ -1024,7 +1032,7 @@ struct evox_cso : Base {
         a.lb = lb_d; a.ub = ub_d; a.lb0 = lb[0]; a.ub0 = ub[0];
         a.uniform_bounds = uniform ? 1 : 0;
         a.rows = rows; a.row0 = row0; a.D = dim; a.ld = ld; a.pop = pop;
-        a.B = B; a.phi = phi; a.xbar = xbar;
+        a.B = B; a.phi = phi; a.xbar = xbar; a.limb = limb;
         a.k0 = (unsigned)(seed & 0xffffffffu);
         a.k1 = (unsigned)(seed >> 32);
         a.rk = evox::Philox::schedule(seed);
@@ -1041,6 +1049,8 @@ struct evox_cso : Base {
                 a.pf[r][0] = pf[r][0];
                 a.pf[r][1] = pf[r][1];
                 a.mbox[r] = pmbox[r];
+                a.plimb[r] = plimb[r];
+                a.pcflag[r] = pcflag[r];
                 a.prow0[r] = prow0[r];
             }
             a.prow0[world] = pop;
@@ -1050,6 +1060,8 @@ struct evox_cso : Base {
             a.pf[0][0] = f2[0];
             a.pf[0][1] = f2[1];
             a.mbox[0] = mbox;
+            a.plimb[0] = limb;
+            a.pcflag[0] = cflag();
             a.prow0[0] = row0;
             a.prow0[1] = row0 + rows;
         }
@@ -1069,8 +1081,9 @@ void cso_layout(evox_cso* s, Carver& c) {
     c.add(&s->ub_d, sizeof(float) * s->ld);
     c.add(&s->ctl, sizeof(Ctl));
     c.add(&s->xbar, sizeof(float) * s->ld);
-    c.add(&s->mbox, (size_t)32 * (s->world > 1 ? s->world : 1));
-    if (s->phi != 0.0f) c.add(&s->colpart, sizeof(double) * s->ld * ((s->rows + 1023) / 1024));
+    // per-generation barrier slots (2 x world x 16 B) + column-sum flags (world x 8 B)
+    c.add(&s->mbox, (size_t)40 * (s->world > 1 ? s->world : 1));
+    if (s->phi != 0.0f) c.add(&s->limb, sizeof(unsigned long long) * 2 * s->ld);
 }
 
 int64_t default_block(int64_t pop) {
@@ -1129,14 +1142,22 @@ evox_status evox_cso_init(int64_t pop, int64_t dim, const float* lb, const float
                         "CSO with world %d and blocks straddling shards (pop=%lld, B=%lld) needs "
                         "global pairing through evox_cso_connect (world <= %d, no workspace)",
                         world, (long long)pop, (long long)B, evox::kMaxPeers);
-        if (phi != 0.0f)
-            return fail(EVOX_ERR_CONFIG, "CSO phi != 0 is supported for world == 1 only");
     }
     evox_cso* s = new (std::nothrow) evox_cso;
     if (!s) return fail(EVOX_ERR_OUT_OF_MEMORY, "host allocation failed");
     s->phi = phi;
     s->B = B;
     s->aligned = aligned;
+    {  // R-15: |x| <= max|bound| <= 2^m  ->  x 2^qs is an integer grid with |q| <= 2^54
+        double m = 0.0;
+        for (int64_t j = 0; j < dim; ++j)
+            m = std::max(m, std::max(std::fabs((double)lb[j]), std::fabs((double)ub[j])));
+        int e = 0;
+        const double fr = std::frexp(m, &e);  // m = fr 2^e, fr in [0.5, 1)
+        if (fr == 0.5) e -= 1;                // exact power of two: 2^(e-1)
+        s->qscale = std::ldexp(1.0, 54 - e);
+        s->qinv = std::ldexp(1.0, e - 54);
+    }
     st = base_setup(s, pop, dim, lb, ub, seed, opts, world, rank);
     if (st == EVOX_OK) {
         Carver c;
@@ -1149,7 +1170,7 @@ evox_status evox_cso_init(int64_t pop, int64_t dim, const float* lb, const float
         cudaError_t e = evox::launch_cso_init(s->args(), s->stream);
         if (e == cudaSuccess) e = cudaMemsetAsync(s->xbar, 0, sizeof(float) * s->ld, s->stream);
         if (e == cudaSuccess)  // peer-barrier flags start at 0 ("nothing published")
-            e = cudaMemsetAsync(s->mbox, 0, (size_t)32 * (s->world > 1 ? s->world : 1), s->stream);
+            e = cudaMemsetAsync(s->mbox, 0, (size_t)40 * (s->world > 1 ? s->world : 1), s->stream);
         if (e == cudaSuccess) e = cudaMalloc(&s->keybuf, sizeof(unsigned long long));
         if (e != cudaSuccess) st = poison(s, EVOX_ERR_CUDA, "cso init", e);
         for (int p = 0; p < 5 && st == EVOX_OK; ++p)
@@ -1194,7 +1215,14 @@ evox_status evox_cso_step(evox_cso* s, evox_problem problem, int64_t n_gens) {
     }
     if (n_gens > 0) {
         st = run_graphed(s, (int)problem, n_gens, [&]() -> evox_status {
-            if (s->phi != 0.0f) CU(s, evox::launch_cso_colmean(a, s->xbar, s->colpart, s->stream));
+            if (s->phi != 0.0f) {  // x-bar of the generation's population (R-15)
+                CU(s, cudaMemsetAsync(s->limb, 0, sizeof(unsigned long long) * 2 * s->ld, s->stream));
+                CU(s, evox::launch_cso_colsum(a, s->qscale, s->stream));
+                if (s->comm && !s->peer)
+                    NC(s, evox::nccl_api(nullptr)->AllReduce(s->limb, s->limb, (size_t)(2 * s->ld),
+                                                            ncclUint64, ncclSum, s->comm, s->stream));
+                CU(s, evox::launch_cso_colmean(a, s->qinv, s->stream));
+            }
             CU(s, timed(s, [&] {
                 return evox::launch_cso_gen((int)problem, a, s->gen_grid[problem], s->stream);
             }));
@@ -1439,6 +1467,8 @@ evox_status evox_cso_connect(evox_cso* s, int mode, const void* peers) {
         s->pf[r][0] = probe.f2[0];
         s->pf[r][1] = probe.f2[1];
         s->pmbox[r] = probe.mbox;
+        s->plimb[r] = probe.limb;
+        s->pcflag[r] = probe.cflag();
         s->prow0[r] = probe.row0;
     }
     st = ensure_hist(s, 1 << 16);  // a step must never synchronise (single-process groups)

@@ -69,7 +69,8 @@ struct CsoArgs {
     long long rows, row0, D, ld, pop;
     long long B;  // pairing block size
     float phi;
-    const float* xbar;  // [ld] column means (phi != 0)
+    float* xbar;               // [ld] column means (phi != 0)
+    unsigned long long* limb;  // [2 x ld] fixed-point column-sum limbs (phi != 0, R-15)
     unsigned int k0, k1;
     PhiloxKey rk;
     Ctl* ctl;
@@ -84,6 +85,8 @@ struct CsoArgs {
     float* pf[kMaxPeers][2];
     long long prow0[kMaxPeers + 1];
     unsigned char* mbox[kMaxPeers];
+    unsigned long long* plimb[kMaxPeers];   // every rank's limbs (phi != 0)
+    unsigned long long* pcflag[kMaxPeers];  // every rank's column-sum flags [world]
     unsigned long long peer_timeout_ns;
 };
 
@@ -137,7 +140,8 @@ cudaError_t launch_cso_init(const CsoArgs& a, cudaStream_t st);
 cudaError_t launch_cso_tell0(const CsoArgs& a, cudaStream_t st);
 int cso_gen_grid(int problem, const CsoArgs& a, int device);
 cudaError_t launch_cso_gen(int problem, const CsoArgs& a, int grid, cudaStream_t st);
-cudaError_t launch_cso_colmean(const CsoArgs& a, float* xbar, double* scratch, cudaStream_t st);
+cudaError_t launch_cso_colsum(const CsoArgs& a, double scale, cudaStream_t st);
+cudaError_t launch_cso_colmean(const CsoArgs& a, double inv_scale, cudaStream_t st);
 cudaError_t launch_cso_hist_from_keys(const CsoArgs& a, unsigned long long t0, long long n,
                                       cudaStream_t st);
 cudaError_t launch_argmin_rows(const float* f, long long rows, long long row0,

@@ -97,9 +97,6 @@ def test_cso_init_validation():
     o.world = 9
     assert L.evox_cso_init(90, 4, lb.ctypes.data, ub.ctypes.data, 0.0, 90, 0, ctypes.byref(o),
                            ctypes.byref(h)) == E.CONFIG
-    o.world = 2
-    assert L.evox_cso_init(100, 4, lb.ctypes.data, ub.ctypes.data, 0.5, 25, 0, ctypes.byref(o),
-                           ctypes.byref(h)) == E.CONFIG  # phi != 0 with world > 1
 
 
 def test_eval_validation():

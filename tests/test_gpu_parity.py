@@ -429,6 +429,25 @@ def test_cso_phi_nonzero_parity():
     assert _cso_parity("sphere", 64, 20, 16, seed=5, gens=10, phi=0.1) <= 1
 
 
+@pytest.mark.parametrize("problem,N,D,B,phi", [("rastrigin", 3000, 37, 3000, 0.3),
+                                               ("griewank", 1030, 130, 10, 0.05)])
+def test_cso_phi_nonzero_parity_many_chunks(problem, N, D, B, phi):
+    """x-bar over several 256-row chunks / CTAs (R-15 fixed-point sums) vs the oracle's
+    fp64 column mean."""
+    assert _cso_parity(problem, N, D, B, seed=11, gens=6, phi=phi) <= 1
+
+
+def test_cso_phi_nccl_path_single_rank(monkeypatch):
+    N, D, p = 256, 40, "ackley"
+    a = ev.CSO(N, D, -32.768, 32.768, phi=0.2, block=32, seed=8)
+    a.step(p, 12)
+    monkeypatch.setenv("EVOX_FORCE_NCCL", "1")
+    b = ev.CSO(N, D, -32.768, 32.768, phi=0.2, block=32, seed=8)
+    b.step(p, 12)
+    assert np.array_equal(a.view("X").cpu().numpy(), b.view("X").cpu().numpy())
+    assert np.array_equal(a.history(), b.history())
+
+
 def test_cso_nccl_path_single_rank(monkeypatch):
     N, D, p = 128, 40, "rastrigin"
     a = ev.CSO(N, D, -5.12, 5.12, block=16, seed=8)
@@ -569,9 +588,9 @@ def test_eval_nonfinite_rows():
 
 
 # ------------------------------------------- CSO global pairing across shards
-def _cso_group(W, N, D, lb, ub, B, seed):
-    hs = [ev.CSO(N, D, lb, ub, block=B, seed=seed, rank=r, world=W, stream=torch.cuda.Stream())
-          for r in range(W)]
+def _cso_group(W, N, D, lb, ub, B, seed, phi=0.0):
+    hs = [ev.CSO(N, D, lb, ub, phi=phi, block=B, seed=seed, rank=r, world=W,
+                 stream=torch.cuda.Stream()) for r in range(W)]
     bases = [h.state_base() for h in hs]
     for h in hs:
         h.connect_local(bases)
@@ -606,6 +625,31 @@ def test_cso_global_pairing_sharded_equals_single(W, N, D, B, problem):
         assert np.array_equal(h.history(), ref.history())
         b = h.best()
         assert b[0] == rb[0] and b[1] == rb[1] and np.array_equal(b[2], rb[2])
+
+
+@pytest.mark.parametrize("W,N,D,B,problem", [(2, 64, 33, 16, "rastrigin"),
+                                             (3, 600, 100, 600, "ackley"),
+                                             (4, 1024, 20, 128, "sphere"),
+                                             (8, 203, 1000, 203, "griewank")])
+def test_cso_phi_sharded_equals_single(W, N, D, B, problem):
+    """phi != 0 with W > 1: each rank sums its rows' fixed-point
+    column limbs, the ranks exchange them through peer memory every generation, and the
+    x-bar -- hence the whole trajectory -- is bitwise the W = 1 run (R-15)."""
+    lb, ub = WL.BOUNDS[problem]
+    ref = ev.CSO(N, D, lb, ub, phi=0.15, block=B, seed=6)
+    ref.step(problem, 12)
+    hs = _cso_group(W, N, D, lb, ub, B, 6, phi=0.15)
+    for h in hs:
+        h.step(problem, 0)
+    for _ in range(3):
+        for h in hs:
+            h.step(problem, 4)
+    for h in hs:
+        h.sync()
+    X = np.concatenate([h.view("X").cpu().numpy()[:, :D] for h in hs])
+    assert np.array_equal(X, ref.view("X").cpu().numpy()[:, :D])
+    for h in hs:
+        assert np.array_equal(h.history(), ref.history())
 
 
 def test_cso_straddling_blocks_require_connect():
