@@ -136,33 +136,14 @@ def ncu_traffic(cfg_name):
 def cpu_baseline(cfg, target_s=12.0):
     """The oracle as it stands, on the host cores, over a bounded row sample of the workload
     (2 generations: move + evaluate + tell), extrapolated to whole-population gens/s."""
-    import oracle as O
     cores = os.cpu_count() or 1
-    lb, ub = WL.BOUNDS[cfg.problem]
     D = cfg.dim
-    # ~54 ns per element per generation per core for PSO (SURVEY App. A.6): size the sample
-    per_elem = 60e-9 / cores
-    rows = int(max(2, min(cfg.pop, target_s / 2 / (per_elem * D * (2 if cfg.algo == "pso" else 1)))))
-    t_gen = None
-    if cfg.algo == "pso":
-        st = O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=0, threads=cores)
-        t0 = time.perf_counter()
-        O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=2, state=st, threads=cores)
-        t_gen = (time.perf_counter() - t0) / 2
-    elif cfg.algo == "de":
-        rows = max(rows, 4)
-        X, f, F64 = O.de_init(cfg.problem, rows, D, lb, ub, 0, threads=cores)
-        t0 = time.perf_counter()
-        for t in range(2):
-            O.de_generation(cfg.problem, X, f, F64, t, 0, lb, ub, threads=cores)
-        t_gen = (time.perf_counter() - t0) / 2
-    else:
-        B = max(2, rows // 8 if rows % 16 == 0 else rows)
-        X, V, f, F64 = O.cso_init(cfg.problem, rows, D, lb, ub, 0, threads=cores)
-        t0 = time.perf_counter()
-        for t in range(2):
-            O.cso_generation(cfg.problem, X, V, f, F64, B, t, 0, lb, ub, threads=cores)
-        t_gen = (time.perf_counter() - t0) / 2
+    rows = _sample_rows(cfg, cores, target_s / 2)
+    gen = _oracle_gen(cfg, rows, cores)
+    t0 = time.perf_counter()
+    for t in range(2):
+        gen(t)
+    t_gen = (time.perf_counter() - t0) / 2
     frac = rows / cfg.pop
     gens_per_s = frac / t_gen
     return {"value": gens_per_s, "unit": "generations/s", "cores": cores, "kind": "oracle",
@@ -171,40 +152,57 @@ def cpu_baseline(cfg, target_s=12.0):
             "individual_dims_per_s": gens_per_s * cfg.pop * D * (0.5 if cfg.algo == "cso" else 1)}
 
 
-def run_reference(args, cfg, rank):
-    if rank != 0:
-        return
+def _oracle_gen(cfg, rows, cores):
+    """Initialise the oracle on `rows` rows of the workload; returns a callable that runs one
+    generation (move + evaluate + tell) in place."""
     import oracle as O
-    cores = os.cpu_count() or 1
     lb, ub = WL.BOUNDS[cfg.problem]
     D = cfg.dim
-    per_elem = 60e-9 / cores
-    budget = 150.0 / max(1, args.steps + args.warmup)  # whole run within a few minutes
-    rows = int(max(2, min(cfg.pop, budget / (per_elem * D * (2 if cfg.algo == "pso" else 1)))))
-    times = []
     if cfg.algo == "pso":
-        st = O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=0, threads=cores)
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            st = O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=1, state=st, threads=cores)
-            if i >= args.warmup:
-                times.append(time.perf_counter() - t0)
+        box = [O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=0, threads=cores)]
+
+        def gen(i):
+            box[0] = O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=1, state=box[0],
+                               threads=cores)
     elif cfg.algo == "de":
-        rows = max(rows, 4)
         X, f, F64 = O.de_init(cfg.problem, rows, D, lb, ub, 0, threads=cores)
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
+
+        def gen(i):
             O.de_generation(cfg.problem, X, f, F64, i, 0, lb, ub, threads=cores)
-            if i >= args.warmup:
-                times.append(time.perf_counter() - t0)
     else:
         B = max(2, rows // 8 if rows % 16 == 0 else rows)
         X, V, f, F64 = O.cso_init(cfg.problem, rows, D, lb, ub, 0, threads=cores)
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
+
+        def gen(i):
             O.cso_generation(cfg.problem, X, V, f, F64, B, i, 0, lb, ub, threads=cores)
-            if i >= args.warmup:
-                times.append(time.perf_counter() - t0)
+    return gen
+
+
+def _sample_rows(cfg, cores, seconds):
+    """Rows of the workload one oracle generation covers in about `seconds` on `cores` threads,
+    calibrated by timing one generation on a small sample (the oracle's speed varies by host)."""
+    rows_c = int(max(4, min(cfg.pop, 2e5 / cfg.dim)))
+    gen = _oracle_gen(cfg, rows_c, cores)
+    t0 = time.perf_counter()
+    gen(0)
+    per_row = max((time.perf_counter() - t0) / rows_c, 1e-12)
+    return int(max(4, min(cfg.pop, seconds / per_row)))
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    D = cfg.dim
+    # whole run (sample init + warm-up + timed generations) within about two minutes
+    rows = _sample_rows(cfg, cores, 90.0 / max(1, args.steps + args.warmup + 1))
+    gen = _oracle_gen(cfg, rows, cores)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        gen(i)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
     value = (rows / cfg.pop) / t
     sample = (f"{rows} of {cfg.pop} rows x dim {D} per step, oracle on {cores} host threads, "
@@ -268,8 +266,11 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nid = None
-    peer = world > 1 and cfg.algo in ("pso", "cso") and args.exchange == "peer"
-    if world > 1 and not peer and cfg.algo != "de":
+    # N>1 exchanges: PSO winner records through in-kernel peer mailboxes (default) or NCCL;
+    # CSO shards connected through IPC-mapped states (default) or NCCL; DE always IPC-mapped
+    peer = world > 1 and cfg.algo == "pso" and args.exchange == "peer"
+    cso_peer = world > 1 and cfg.algo == "cso" and args.exchange == "peer"
+    if world > 1 and not peer and not cso_peer and cfg.algo != "de":
         buf = torch.zeros(128, dtype=torch.uint8, device=cdev)
         if rank == 0:
             buf.copy_(torch.frombuffer(bytearray(ev.nccl_unique_id()), dtype=torch.uint8))
@@ -293,7 +294,7 @@ def main():
     elif cfg.algo == "cso":  # N>1: shards connected through IPC-mapped states (peer barrier)
         h = ev.CSO(cfg.pop, cfg.dim, lb, ub, block=cfg.pop // 8 if cfg.pop % 16 == 0 else 0,
                    seed=0, rank=rank, world=world, nccl_id=nid)
-        if world > 1 and args.exchange == "peer":
+        if cso_peer:
             mine = torch.frombuffer(bytearray(h.state_ipc()), dtype=torch.uint8).to(cdev)
             allh = [torch.zeros(64, dtype=torch.uint8, device=cdev) for _ in range(world)]
             dist.all_gather(allh, mine)
@@ -372,7 +373,7 @@ def main():
             "config": {"workload": cfg.note, "algo": cfg.algo, "problem": cfg.problem,
                        "pop": cfg.pop, "dim": cfg.dim, "seed": 0,
                        "parallelism": f"row-sharded x{world}" + (
-                           f", exchange={'peer-memory (in-kernel)' if peer else ('peer-memory donors' if cfg.algo == 'de' else 'nccl')}"
+                           f", exchange={'peer-memory (in-kernel)' if peer else ('peer-memory donors' if cfg.algo == 'de' else ('peer-memory pairs' if cso_peer else 'nccl'))}"
                            if world > 1 else ""),
                        "l2": "state (X,V,P) > L2: inputs larger than L2, no flush needed"
                        if 12 * cfg.pop * cfg.dim > 2 * 126e6 else "state comparable to L2"},

@@ -458,6 +458,11 @@ inline int grid_for(const void* fn, long long units, int device) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
     if (per_sm < 1) per_sm = 1;
     long long g = (long long)sm_count(device) * per_sm;
+    // EVOX_NP=k: k waves of resident CTAs (k = 0: one CTA per row unit)
+    if (const char* np = getenv("EVOX_NP")) {
+        const long long k = atoll(np);
+        g = k <= 0 ? units : g * k;
+    }
     if (units < g) g = units;
     return (int)(g < 1 ? 1 : g);
 }
