@@ -229,7 +229,7 @@ def main():
     ap.add_argument("--config", default="H", choices=sorted(WL.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--pop", type=int, default=0, help="override the population (profiling only)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="PSO winner exchange for N>1: in-kernel over NVLink peer memory "
@@ -283,31 +283,38 @@ def main():
         torch.cuda.synchronize()
 
     lb, ub = WL.BOUNDS[cfg.problem]
-    if cfg.algo == "de":  # shards read donors across GPUs: map every rank's state (IPC)
-        h = ev.DE(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world)
-        if world > 1:
-            mine = torch.frombuffer(bytearray(h.state_ipc()), dtype=torch.uint8).to(cdev)
+
+    def open_handle():
+        """Handle setup through the public API: init from host lb/ub (copied H2D by the
+        C-ABI), X0 from the seed on the device, N>1 peer mapping."""
+        if cfg.algo == "de":  # shards read donors across GPUs: map every rank's state (IPC)
+            h = ev.DE(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world)
+            if world > 1:
+                mine = torch.frombuffer(bytearray(h.state_ipc()), dtype=torch.uint8).to(cdev)
+                allh = [torch.zeros(64, dtype=torch.uint8, device=cdev) for _ in range(world)]
+                dist.all_gather(allh, mine)
+                h.connect_ipc([bytes(x.cpu().numpy().tobytes()) for x in allh])
+                barrier()
+        elif cfg.algo == "cso":  # N>1: shards connected through IPC-mapped states (peer barrier)
+            h = ev.CSO(cfg.pop, cfg.dim, lb, ub, block=cfg.pop // 8 if cfg.pop % 16 == 0 else 0,
+                       seed=0, rank=rank, world=world, nccl_id=nid)
+            if cso_peer:
+                mine = torch.frombuffer(bytearray(h.state_ipc()), dtype=torch.uint8).to(cdev)
+                allh = [torch.zeros(64, dtype=torch.uint8, device=cdev) for _ in range(world)]
+                dist.all_gather(allh, mine)
+                h.connect_ipc([bytes(x.cpu().numpy().tobytes()) for x in allh])
+                barrier()
+        else:
+            h = ev.PSO(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world, nccl_id=nid)
+        if peer:  # mailboxes of all ranks mapped into every rank through CUDA IPC
+            mine = torch.frombuffer(bytearray(h.mailbox_ipc()), dtype=torch.uint8).to(cdev)
             allh = [torch.zeros(64, dtype=torch.uint8, device=cdev) for _ in range(world)]
             dist.all_gather(allh, mine)
             h.connect_ipc([bytes(x.cpu().numpy().tobytes()) for x in allh])
             barrier()
-    elif cfg.algo == "cso":  # N>1: shards connected through IPC-mapped states (peer barrier)
-        h = ev.CSO(cfg.pop, cfg.dim, lb, ub, block=cfg.pop // 8 if cfg.pop % 16 == 0 else 0,
-                   seed=0, rank=rank, world=world, nccl_id=nid)
-        if cso_peer:
-            mine = torch.frombuffer(bytearray(h.state_ipc()), dtype=torch.uint8).to(cdev)
-            allh = [torch.zeros(64, dtype=torch.uint8, device=cdev) for _ in range(world)]
-            dist.all_gather(allh, mine)
-            h.connect_ipc([bytes(x.cpu().numpy().tobytes()) for x in allh])
-            barrier()
-    else:
-        h = ev.PSO(cfg.pop, cfg.dim, lb, ub, seed=0, rank=rank, world=world, nccl_id=nid)
-    if peer:  # mailboxes of all ranks mapped into every rank through CUDA IPC
-        mine = torch.frombuffer(bytearray(h.mailbox_ipc()), dtype=torch.uint8).to(cdev)
-        allh = [torch.zeros(64, dtype=torch.uint8, device=cdev) for _ in range(world)]
-        dist.all_gather(allh, mine)
-        h.connect_ipc([bytes(x.cpu().numpy().tobytes()) for x in allh])
-        barrier()
+        return h
+
+    h = open_handle()
     rows = h.info()["rows"]
     stream = h.stream
     h.step(cfg.problem, 0)          # generation 0: evaluate X0 + tell
@@ -337,18 +344,26 @@ def main():
     ms_total, k_avg_ms = float(t[0]), float(t[1])
     ms_per_step = ms_total / args.steps
 
-    # ---- end to end through the public API: step + D2H of the step's result, every step
-    import numpy as np
+    # ---- end to end: one whole job through the public API with host buffers, timed by the
+    # host clock (max over ranks): init from host lb/ub (H2D inside the C-ABI), X0 from the
+    # seed, generation 0, then every step evox_*_step(1) + a synchronising best() D2H of the
+    # step's result (fitness, global index, best row), and the per-generation history D2H.
+    h.close()
     barrier()
     t0 = time.perf_counter()
+    h = open_handle()
+    h.step(cfg.problem, 0)
     for _ in range(args.e2e_steps):
         h.step(cfg.problem, 1)
-        best = h.best(with_row=True)  # synchronising D2H: fitness, index, best row
+        best = h.best(with_row=True)
+    hist = h.history()
     e2e_s = time.perf_counter() - t0
     e2e = torch.tensor([e2e_s], dtype=torch.float64, device=cdev)
     if launched:
         dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     e2e_s = float(e2e[0])
+    e2e_h2d = 2 * 4 * cfg.dim / args.e2e_steps            # lb, ub (per job, amortised)
+    e2e_d2h = (4 + 8 + 4 * cfg.dim) + 4 * len(hist) / args.e2e_steps
 
     if rank == 0:
         peak, peak_src = hbm_peak()
@@ -389,9 +404,13 @@ def main():
             "gpu_launches": k_launch + (args.steps if (cfg.algo == "pso" and world > 1
                                                        and not peer) else 0),
             "e2e": {"value": args.e2e_steps / e2e_s, "unit": "generations/s",
-                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 + 8 + 4 * cfg.dim,
-                    "note": "per step: evox_*_step(1) through the C-ABI + synchronising "
-                            "best() D2H (fitness, index, best row) into host memory"},
+                    "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
+                    "steps": args.e2e_steps,
+                    "note": "host clock over one whole job through the C-ABI: init from host "
+                            "lb/ub (H2D; the population is the method's own Philox init from "
+                            "the seed, R-3), generation 0, then per step evox_*_step(1) + "
+                            "synchronising best() D2H (fitness, index, best row), and the "
+                            "history D2H; job setup amortised over the steps"},
         }
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(cfg)
