@@ -257,7 +257,7 @@ cudaError_t launch_de_tell0(const DeArgs& a, cudaStream_t st) {
 int de_gen_grid(int problem, long long ld, long long rows, int device) {
     int g = 1;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
-        g = grid_for((const void*)k_de_gen<P_, G_, true>, row_units<G_>(rows), device);
+        g = grid_for((const void*)k_de_gen<P_, G_, true>, row_units<G_>(rows), device, 16);
     }));
     return g;
 }

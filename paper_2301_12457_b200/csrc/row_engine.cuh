@@ -446,6 +446,13 @@ using GW8 = Geom<32, 8, 3>;  // long rows: 3 chunks in flight measured best (C5)
 // row (ld <= 4096), 2: a CTA per row.  Narrow row groups keep short rows from
 // idling lanes (dim 100 = 25 quads: 28 lane-slots with 4 lanes vs 32 with 8).
 inline int geom_id(long long ld) {
+    // EVOX_GEOM=id forces one geometry for every launch of the process (tuning sweeps only:
+    // results stay exact, but reduction orders -- hence fitness bits -- follow the geometry)
+    static const int forced = [] {
+        const char* g = getenv("EVOX_GEOM");
+        return g && *g ? atoi(g) : -1;
+    }();
+    if (forced >= 0 && forced <= 3) return forced;
     const long long NQ = ld >> 2;
     if (NQ <= 32) return 3;
     if (NQ <= 64) return 0;
@@ -453,15 +460,17 @@ inline int geom_id(long long ld) {
     return 2;
 }
 
-inline int grid_for(const void* fn, long long units, int device) {
+// `waves` x (resident CTAs): 1 = persistent grid-stride (PSO, CSO: measured best); the DE
+// generation takes 16 (pop 1e6 x dim 100: +14 %, neutral at dim 1000).
+inline int grid_for(const void* fn, long long units, int device, int waves = 1) {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
     if (per_sm < 1) per_sm = 1;
-    long long g = (long long)sm_count(device) * per_sm;
+    long long g = (long long)sm_count(device) * per_sm * waves;
     // EVOX_NP=k: k waves of resident CTAs (k = 0: one CTA per row unit)
     if (const char* np = getenv("EVOX_NP")) {
         const long long k = atoll(np);
-        g = k <= 0 ? units : g * k;
+        g = k <= 0 ? units : (long long)sm_count(device) * per_sm * k;
     }
     if (units < g) g = units;
     return (int)(g < 1 ? 1 : g);
