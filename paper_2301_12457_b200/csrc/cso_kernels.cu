@@ -398,14 +398,14 @@ static long long cso_items(const CsoArgs& a) {
 
 int cso_gen_grid(int problem, const CsoArgs& a, int device) {
     int g = 1;
-    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+    EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM_ID(cso_geom_id(a.ld), {
         g = grid_for((const void*)k_cso_gen<P_, G_, true>, row_units<G_>(cso_items(a)), device);
     }));
     return g;
 }
 
 cudaError_t launch_cso_gen(int problem, const CsoArgs& a, int grid, cudaStream_t st) {
-    EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+    EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM_ID(cso_geom_id(a.ld), {
         k_cso_gen<P_, G_, U_><<<grid, 256, 0, st>>>(a);
     })));
     return cudaGetLastError();

@@ -462,6 +462,14 @@ inline int geom_id(long long ld) {
 
 // `waves` x (resident CTAs): 1 = persistent grid-stride (PSO, CSO: measured best); the DE
 // generation takes 16 (pop 1e6 x dim 100: +14 %, neutral at dim 1000).
+// CSO generation: 8 lanes per row up to 1024 quads (one warp walks 4 independent pairs at
+// once, so more scattered winner/loser rows are in flight: C3 71 -> 77 % of HBM peak; PSO
+// and DE measured worse with it). Still a function of ld only (R-11).
+inline int cso_geom_id(long long ld) {
+    const int g = geom_id(ld);
+    return g == 1 && getenv("EVOX_GEOM") == nullptr ? 0 : g;
+}
+
 inline int grid_for(const void* fn, long long units, int device, int waves = 1) {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
@@ -500,9 +508,10 @@ inline long long row_units(long long rows) {
 
 }  // namespace
 
-#define EVOX_DISPATCH_GEOM(ld, ...)     \
+#define EVOX_DISPATCH_GEOM(ld, ...) EVOX_DISPATCH_GEOM_ID(geom_id(ld), __VA_ARGS__)
+#define EVOX_DISPATCH_GEOM_ID(id, ...)  \
     do {                                \
-        switch (geom_id(ld)) {          \
+        switch (id) {                   \
             case 3: {                   \
                 using G_ = G4;          \
                 __VA_ARGS__;            \

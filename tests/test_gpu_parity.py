@@ -664,7 +664,8 @@ def test_cso_straddling_blocks_require_connect():
 def test_fused_fitness_equals_evaluate(problem, N, D, monkeypatch):
     """the fitness the fused generation kernel computes from registers is
     bitwise the standalone Problem.evaluate of the same population (same per-row
-    reduction order: a function of dim only)."""
+    reduction order: a function of dim only) -- for CSO whenever its row geometry is
+    evaluate's (else within the fitness tolerance)."""
     lb, ub = WL.BOUNDS[problem]
     monkeypatch.setenv("EVOX_NO_SMALL", "1")
     pso = ev.PSO(N, D, lb, ub, seed=1)
@@ -675,7 +676,13 @@ def test_fused_fitness_equals_evaluate(problem, N, D, monkeypatch):
     cso = ev.CSO(N + N % 2, D, lb, ub, seed=1)
     cso.step(problem, 2)
     f = ev.evaluate(problem, cso.view("X").clone(), dim=D).cpu().numpy()
-    assert np.array_equal(f, cso.view("F").cpu().numpy())
+    if 64 < (D + 3) // 4 <= 1024:
+        # the CSO generation walks these rows with 8 lanes per row (evaluate: a warp per
+        # row), so only the reduction order differs: equal within the fitness tolerance
+        fc = cso.view("F").cpu().numpy()
+        assert (np.abs(fc - f) <= np.maximum(1e-5 * np.abs(f), 1e-6)).all()
+    else:
+        assert np.array_equal(f, cso.view("F").cpu().numpy())
     de = ev.DE(N, D, lb, ub, seed=1)
     de.step(problem, 2)
     f = ev.evaluate(problem, de.view("X").clone(), dim=D).cpu().numpy()
