@@ -229,7 +229,7 @@ def main():
     ap.add_argument("--config", default="H", choices=sorted(WL.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--pop", type=int, default=0, help="override the population (profiling only)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="PSO winner exchange for N>1: in-kernel over NVLink peer memory "
