@@ -114,7 +114,9 @@ evox_status evox_nccl_unique_id(uint8_t out[128]);
  * i < pop.  X: dev [pop x ld] f32 (ld >= dim, ld % 4 == 0, 16-byte aligned);
  * fit: dev [pop] f32.  Row-wise pure: fit[i] depends only on row i,
  * with a reduction order fixed by dim alone.  Asynchronous on cuda_stream
- * (NULL = legacy default stream).  pop == 0 is a no-op. */
+ * (NULL = legacy default stream).  pop == 0 is a no-op.  ld > 2^31 - 4 ->
+ * EVOX_ERR_SHAPE (in-row indices are 32-bit; the same cap applies to dim at
+ * every init). */
 evox_status evox_eval(evox_problem problem, const float* X, int64_t pop, int64_t dim, int64_t ld,
                       float* fit, void* cuda_stream);
 

@@ -61,7 +61,7 @@ struct MoverCso {
     float4 x[U], v[U], xw[U];
     __device__ __forceinline__ MoverCso(const CsoArgs& a_) : a(a_) {}
     template <bool EF>
-    __device__ __forceinline__ void load(int u, long long q) {
+    __device__ __forceinline__ void load(int u, int q) {
         x[u] = ld_stream<EF>(Xl + q);
         v[u] = ld_stream<EF>(Vl + q);
         xw[u] = ld_stream<EF>(Xw + q);
@@ -74,7 +74,7 @@ struct MoverCso {
         vout = v;
         return clipf(__fadd_rn(xl, v), lo, hi);
     }
-    __device__ __forceinline__ float4 step(int u, long long q) {
+    __device__ __forceinline__ float4 step(int u, int q) {
         const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 5u), a.rk);
         const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 6u), a.rk);
         const bool use3 = a.phi != 0.0f;

@@ -51,7 +51,7 @@ struct MoverDe {
     float4 x[U], xa[U], xb[U], xc[U];
     __device__ __forceinline__ explicit MoverDe(const DeArgs& a_) : a(a_) {}
     template <bool EF>
-    __device__ __forceinline__ void load(int u, long long q) {
+    __device__ __forceinline__ void load(int u, int q) {
         x[u] = ld_stream<EF>(Xi + q);
         xa[u] = __ldcg(Xa + q);  // donors: random rows, may be re-read by other targets
         xb[u] = __ldcg(Xb + q);
@@ -64,7 +64,7 @@ struct MoverDe {
         const float y = (U < CR || forced) ? v : xi;
         return clipf(y, lo, hi);
     }
-    __device__ __forceinline__ float4 step(int u, long long q) {
+    __device__ __forceinline__ float4 step(int u, int q) {
         const uint4 b = Philox::run(make_uint4((uint32_t)q, row_g, t, 10u), a.rk);
         const float4 lo = bound4t<UNI>(a.lb, a.lb0, q);
         const float4 hi = bound4t<UNI>(a.ub, a.ub0, q);

@@ -38,6 +38,7 @@ evox_status fail(evox_status st, const char* fmt, ...) {
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 int64_t round4(int64_t d) { return (d + 3) / 4 * 4; }
+constexpr int64_t MAX_LD = 0x7FFFFFFCll;  // ld <= 2^31 - 4: in-row quad / column indices fit int32
 
 bool mul_ok(int64_t a, int64_t b, int64_t lim) { return a >= 0 && b >= 0 && (b == 0 || a <= lim / b); }
 
@@ -551,6 +552,7 @@ evox_status evox_eval(evox_problem problem, const float* X, int64_t pop, int64_t
     if (!valid_problem(problem)) return fail(EVOX_ERR_INVALID_ARGUMENT, "unknown problem %d", (int)problem);
     if (pop < 0 || dim < 1) return fail(EVOX_ERR_SHAPE, "need pop >= 0 and dim >= 1");
     if (ld < dim || ld % 4) return fail(EVOX_ERR_SHAPE, "ld must be >= dim and a multiple of 4");
+    if (ld > MAX_LD) return fail(EVOX_ERR_SHAPE, "ld must be <= 2^31 - 4 (in-row indices are 32-bit)");
     if (!mul_ok(pop, ld, INT64_MAX / 4)) return fail(EVOX_ERR_SHAPE, "pop*ld overflows");
     if (pop == 0) return EVOX_OK;
     if (!X || !fit) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL X or fit");
@@ -585,7 +587,7 @@ evox_status evox_pso_init(int64_t pop, int64_t dim, const float* lb, const float
     if (pop < 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "pop must be >= 1 (got %lld)", (long long)pop);
     if (dim < 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "dim must be >= 1 (got %lld)", (long long)dim);
     if (pop > 0xFFFFFFFFll) return fail(EVOX_ERR_SHAPE, "pop must be < 2^32 (Philox row counter)");
-    if (round4(dim) / 4 > 0xFFFFFFFFll) return fail(EVOX_ERR_SHAPE, "dim too large");
+    if (round4(dim) > MAX_LD) return fail(EVOX_ERR_SHAPE, "dim must be <= 2^31 - 4 (in-row indices are 32-bit)");
     if (!mul_ok(pop, round4(dim), INT64_MAX / 64)) return fail(EVOX_ERR_SHAPE, "pop*dim overflows");
     if (!std::isfinite(w) || !std::isfinite(phi_p) || !std::isfinite(phi_g))
         return fail(EVOX_ERR_INVALID_ARGUMENT, "w, phi_p, phi_g must be finite");
@@ -1125,6 +1127,7 @@ evox_status evox_cso_init(int64_t pop, int64_t dim, const float* lb, const float
     if (pop < 2) return fail(EVOX_ERR_INVALID_ARGUMENT, "CSO needs pop >= 2 (got %lld)", (long long)pop);
     if (dim < 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "dim must be >= 1");
     if (pop > 0xFFFFFFFFll) return fail(EVOX_ERR_SHAPE, "pop must be < 2^32");
+    if (round4(dim) > MAX_LD) return fail(EVOX_ERR_SHAPE, "dim must be <= 2^31 - 4 (in-row indices are 32-bit)");
     if (!mul_ok(pop, round4(dim), INT64_MAX / 64)) return fail(EVOX_ERR_SHAPE, "pop*dim overflows");
     if (!std::isfinite(phi)) return fail(EVOX_ERR_INVALID_ARGUMENT, "phi must be finite");
     if (block < 0 || block == 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "block must be 0 (default) or >= 2");
@@ -1626,6 +1629,7 @@ evox_status evox_de_init(int64_t pop, int64_t dim, const float* lb, const float*
     if (pop < 4) return fail(EVOX_ERR_CONFIG, "DE needs pop >= 4 (got %lld; S:326)", (long long)pop);
     if (dim < 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "dim must be >= 1");
     if (pop > 0xFFFFFFFFll) return fail(EVOX_ERR_SHAPE, "pop must be < 2^32");
+    if (round4(dim) > MAX_LD) return fail(EVOX_ERR_SHAPE, "dim must be <= 2^31 - 4 (in-row indices are 32-bit)");
     if (!mul_ok(pop, round4(dim), INT64_MAX / 64)) return fail(EVOX_ERR_SHAPE, "pop*dim overflows");
     if (!std::isfinite(F)) return fail(EVOX_ERR_INVALID_ARGUMENT, "F must be finite");
     if (!(CR >= 0.0f && CR <= 1.0f)) return fail(EVOX_ERR_INVALID_ARGUMENT, "CR must be in [0,1]");

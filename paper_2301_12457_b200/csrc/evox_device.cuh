@@ -229,7 +229,7 @@ template <> struct Fit<ROSENBROCK> {
 // folds the three intra-quad pairs (the pair crossing into the next quad is
 // handled by the row engine with a shuffle / carried value).
 template <int P>
-__device__ __forceinline__ void fit_quad(Fit<P>& acc, float4 x, int64_t j0, int64_t D,
+__device__ __forceinline__ void fit_quad(Fit<P>& acc, float4 x, int j0, int D,
                                          const float* = nullptr) {
     if (j0 + 3 < D) {
         acc.elem(x.x, j0); acc.elem(x.y, j0 + 1); acc.elem(x.z, j0 + 2); acc.elem(x.w, j0 + 3);
@@ -240,8 +240,8 @@ __device__ __forceinline__ void fit_quad(Fit<P>& acc, float4 x, int64_t j0, int6
     }
 }
 template <>
-__device__ __forceinline__ void fit_quad<GRIEWANK>(Fit<GRIEWANK>& acc, float4 x, int64_t j0,
-                                                   int64_t D, const float* htab) {
+__device__ __forceinline__ void fit_quad<GRIEWANK>(Fit<GRIEWANK>& acc, float4 x, int j0,
+                                                   int D, const float* htab) {
     float4 h;
     if (htab) {
         h = *reinterpret_cast<const float4*>(htab + j0);  // LDS.128 of the column constants
@@ -258,8 +258,8 @@ __device__ __forceinline__ void fit_quad<GRIEWANK>(Fit<GRIEWANK>& acc, float4 x,
     }
 }
 template <>
-__device__ __forceinline__ void fit_quad<ROSENBROCK>(Fit<ROSENBROCK>& acc, float4 x, int64_t j0,
-                                                     int64_t D, const float*) {
+__device__ __forceinline__ void fit_quad<ROSENBROCK>(Fit<ROSENBROCK>& acc, float4 x, int j0,
+                                                     int D, const float*) {
     if (j0 + 1 < D) acc.pair(x.x, x.y);
     if (j0 + 2 < D) acc.pair(x.y, x.z);
     if (j0 + 3 < D) acc.pair(x.z, x.w);

@@ -37,12 +37,12 @@ struct MoverPso {
         pend = pend_;
     }
     template <bool EF>
-    __device__ __forceinline__ void load(int u, long long q) {
+    __device__ __forceinline__ void load(int u, int q) {
         x[u] = ld_stream<EF>(Xr + q);
         v[u] = ld_stream<EF>(Vr + q);
         if (!pend) p[u] = ld_stream<EF>(Pr + q);
     }
-    __device__ __forceinline__ float4 step(int u, long long q) {
+    __device__ __forceinline__ float4 step(int u, int q) {
         const float4 xo = x[u];
         const float4 pb = pend ? xo : p[u];
         if (pend) st_stream(Pr + q, xo);

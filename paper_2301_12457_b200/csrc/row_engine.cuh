@@ -85,7 +85,7 @@ __device__ __forceinline__ float4 bound4(const float* b, float b0, int uniform, 
 // Compile-time specialisation: uniform bounds feed FMNMX straight from the
 // constant bank; per-column bounds are two L1-resident LDG.128 per quad.
 template <bool UNI>
-__device__ __forceinline__ float4 bound4t(const float* b, float b0, long long q) {
+__device__ __forceinline__ float4 bound4t(const float* b, float b0, int q) {
     if constexpr (UNI) return make_float4(b0, b0, b0, b0);
     else return __ldg(reinterpret_cast<const float4*>(b) + q);
 }
@@ -113,9 +113,9 @@ __device__ __forceinline__ void pso_elem(float& x, float& v, float p, float g, f
     v = vn;
 }
 
-__device__ __forceinline__ void zero_pad(float4& x, float4& v, long long q, long long D) {
+__device__ __forceinline__ void zero_pad(float4& x, float4& v, int q, int D) {
     if (4 * q + 3 >= D) {  // padding columns stay 0
-        const long long j0 = 4 * q;
+        const int j0 = 4 * q;
         if (j0 + 1 >= D) { x.y = 0.f; v.y = 0.f; }
         if (j0 + 2 >= D) { x.z = 0.f; v.z = 0.f; }
         if (j0 + 3 >= D) { x.w = 0.f; v.w = 0.f; }
@@ -187,28 +187,31 @@ struct NoPrefetch {
 // iteration (qb/qe are warp-uniform); lanes of an absent row (`row_ok` false)
 // do no memory work.  `pf(base)` is called by the warp at each group start.
 template <int P, class G, class Mover, class PF>
-__device__ __forceinline__ void walk_segment(Mover& mv, long long qb, long long qe, long long D,
+__device__ __forceinline__ void walk_segment(Mover& mv, long long qb_, long long qe_, long long D_,
                                              bool row_ok, Fit<P>& acc, float& head_x,
                                              float& tail_x, bool& tail_valid, PF& pf,
                                              const float* htab = nullptr) {
+    // in-row indices in 32 bits (ld < 2^31 is validated at init): fewer integer
+    // instructions per chunk than 64-bit compares and adds
     const int sl = lane_id() & (G::LPR - 1);
+    const int qb = (int)qb_, qe = (int)qe_, D = (int)D_;
     float pend_x = 0.0f;
     bool pend = false;  // last sub-lane: x_{4q+3} waiting for x_{4q+4} of the next chunk
     head_x = 0.0f;
     tail_valid = false;
     tail_x = 0.0f;
-    for (long long base = qb; base < qe; base += G::GROUP) {
+    for (int base = qb; base < qe; base += G::GROUP) {
         pf(base);
 #pragma unroll
         for (int u = 0; u < G::NU; ++u) {
-            const long long q = base + G::LPR * u + sl;
+            const int q = base + G::LPR * u + sl;
             if (row_ok && q < qe) mv.template load<G::EFL>(u, q);
         }
 #pragma unroll
         for (int u = 0; u < G::NU; ++u) {
-            const long long cb = base + G::LPR * u;  // first quad of this chunk
+            const int cb = base + G::LPR * u;  // first quad of this chunk
             if (cb >= qe) break;                     // warp-uniform
-            const long long q = cb + sl;
+            const int q = cb + sl;
             const bool valid = row_ok && q < qe;
             float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
             if (valid) {
@@ -313,7 +316,7 @@ struct MoverEval {
     const float4* Xr;
     float4 x[U];
     template <bool EF>
-    __device__ __forceinline__ void load(int u, long long q) { x[u] = ld_stream<EF>(Xr + q); }
+    __device__ __forceinline__ void load(int u, int q) { x[u] = ld_stream<EF>(Xr + q); }
     __device__ __forceinline__ float4 step(int u, long long) { return x[u]; }
 };
 
