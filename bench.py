@@ -58,8 +58,11 @@ def algorithmic_bytes(cfg, rows):
     imp r+w (2), pf read (4), f write (4) = 10 B (the rare pf write is not counted).
     CSO: per loser element Xl r+w, Vl r+w, Xw read = 20 B, i.e. 10 B per population
     element; per pair f reads (8) + loser f write (4) = 6 B per row.
-    DE: per element the target and three donor rows read (16) + the trial written (4)."""
+    DE: per element the target and three donor rows read (16) + the trial written (4).
+    eval: X read (4 B/element) + f written (4 B/row)."""
     D = cfg.dim
+    if cfg.algo == "eval":  # Problem.evaluate: read X (4 B/element), write f (4 B/row)
+        return 4 * D * rows + 4 * rows
     if cfg.algo == "pso":
         return 20 * D * rows + 10 * rows
     if cfg.algo == "de":  # target 4 + three donors 12 + trial write 4; sel 4+1, f 4+4 per row
@@ -146,10 +149,115 @@ def cpu_baseline(cfg, target_s=12.0):
     t_gen = (time.perf_counter() - t0) / 2
     frac = rows / cfg.pop
     gens_per_s = frac / t_gen
-    return {"value": gens_per_s, "unit": "generations/s", "cores": cores, "kind": "oracle",
-            "sample": f"{rows} of {cfg.pop} rows x dim {D}, 2 generations (move+eval+tell), "
+    what = "2 evaluations" if cfg.algo == "eval" else "2 generations (move+eval+tell)"
+    return {"value": gens_per_s, "unit": _unit(cfg), "cores": cores, "kind": "oracle",
+            "sample": f"{rows} of {cfg.pop} rows x dim {D}, {what}, "
                       f"{t_gen * 2:.2f} s; extrapolated linearly in rows",
             "individual_dims_per_s": gens_per_s * cfg.pop * D * (0.5 if cfg.algo == "cso" else 1)}
+
+
+def _unit(cfg):
+    return "populations evaluated/s" if cfg.algo == "eval" else "generations/s"
+
+
+def run_eval(args, cfg, world, rank, local):
+    """SURVEY §8(d) `evox_eval` line: one step = Problem.evaluate (Eq. (2)) of the whole
+    population through the C-ABI -- this rank's contiguous row shard at N > 1 (rows are
+    independent: no collective, weak in nothing but the shard).  X ~ U[lb, ub] (seeded torch
+    generator: plumbing, not the method), padding columns 0, resident in HBM."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_12457_b200 as ev
+    torch.cuda.set_device(local)
+    launched = "WORLD_SIZE" in os.environ
+    if launched:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if launched:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    row0, rows = ev.shard_rows(cfg.pop, world, rank)
+    D, ld = cfg.dim, WL.round4(cfg.dim)
+    lb, ub = WL.BOUNDS[cfg.problem]
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1000 + rank)
+    X = torch.zeros((rows, ld), dtype=torch.float32, device="cuda")
+    X[:, :D].uniform_(lb, ub, generator=gen)
+    f = torch.empty(rows, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.Stream()
+    for _ in range(args.warmup):
+        ev.evaluate(cfg.problem, X, dim=D, out=f, stream=stream)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for k in range(args.steps):
+        ev.evaluate(cfg.problem, X, dim=D, out=f, stream=stream)
+        evs[k + 1].record(stream)
+    stream.synchronize()
+    barrier()
+    clk = clocks.stop()
+    per = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    t = torch.tensor([sum(per), sum(per) / len(per)], dtype=torch.float64, device="cuda")
+    if launched:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t[0]) / args.steps
+    k_avg_ms = float(t[1])
+
+    # e2e through the C-ABI with host buffers: pinned host X -> device, evaluate, fitness -> host
+    Xh = X.cpu().pin_memory()
+    fh = torch.empty(rows, dtype=torch.float32).pin_memory()
+    n_e2e = max(1, min(args.e2e_steps, 5))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        with torch.cuda.stream(stream):
+            X.copy_(Xh, non_blocking=True)
+            ev.evaluate(cfg.problem, X, dim=D, out=f, stream=stream)
+            fh.copy_(f, non_blocking=True)
+        stream.synchronize()
+    e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    if launched:
+        dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e[0])
+
+    if rank == 0:
+        peak, peak_src = hbm_peak()
+        bytes_launch = algorithmic_bytes(cfg, rows)
+        achieved = bytes_launch / (k_avg_ms * 1e-3) / 1e9
+        value = 1e3 / ms_per_step
+        line = {
+            "metric": METRIC, "value": value, "unit": _unit(cfg), "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.note, "algo": "eval", "problem": cfg.problem,
+                       "pop": cfg.pop, "dim": cfg.dim, "seed": 1000,
+                       "parallelism": f"row-sharded x{world}",
+                       "l2": "X (4 GB) > L2: inputs larger than L2, no flush needed"},
+            "individual_dims_per_s": value * cfg.pop * cfg.dim,
+            "bytes_per_generation": algorithmic_bytes(cfg, cfg.pop),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                         "kernel": f"k_eval<{cfg.problem}>", "kernel_ms": k_avg_ms,
+                         "bytes_per_launch": bytes_launch, "peak_source": peak_src},
+            "clocks": clk,
+            "gpu_launches": args.steps,
+            "e2e": {"value": n_e2e / e2e_s, "unit": _unit(cfg),
+                    "h2d_bytes_per_step": 4 * cfg.pop * ld, "d2h_bytes_per_step": 4 * cfg.pop,
+                    "steps": n_e2e,
+                    "note": "per step: pinned host X -> device, evox_eval through the C-ABI, "
+                            "fitness -> pinned host, stream sync"},
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line), flush=True)
+    if launched:
+        dist.destroy_process_group()
 
 
 def _oracle_gen(cfg, rows, cores):
@@ -158,7 +266,12 @@ def _oracle_gen(cfg, rows, cores):
     import oracle as O
     lb, ub = WL.BOUNDS[cfg.problem]
     D = cfg.dim
-    if cfg.algo == "pso":
+    if cfg.algo == "eval":
+        X = WL.uniform_rows(rows, D, cfg.problem, seed=0)
+
+        def gen(i):
+            O.evaluate(cfg.problem, X, threads=cores)
+    elif cfg.algo == "pso":
         box = [O.pso_run(cfg.problem, rows, D, lb, ub, seed=0, n_gens=0, threads=cores)]
 
         def gen(i):
@@ -207,16 +320,16 @@ def run_reference(args, cfg, rank):
     value = (rows / cfg.pop) / t
     sample = (f"{rows} of {cfg.pop} rows x dim {D} per step, oracle on {cores} host threads, "
               f"extrapolated linearly in rows")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "generations/s",
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": _unit(cfg),
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t * 1e3 * cfg.pop / rows, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.note, "algo": cfg.algo, "problem": cfg.problem,
                        "pop": cfg.pop, "dim": cfg.dim},
             "individual_dims_per_s": value * cfg.pop * D * (0.5 if cfg.algo == "cso" else 1),
-            "cpu_baseline": {"value": value, "unit": "generations/s", "cores": cores,
+            "cpu_baseline": {"value": value, "unit": _unit(cfg), "cores": cores,
                              "kind": "oracle", "sample": sample},
-            "e2e": {"value": value, "unit": "generations/s", "h2d_bytes_per_step": 0,
+            "e2e": {"value": value, "unit": _unit(cfg), "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -246,6 +359,8 @@ def main():
     local = _env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         return run_reference(args, cfg, rank)
+    if cfg.algo == "eval":
+        return run_eval(args, cfg, world, rank, local)
 
     import torch
     import torch.distributed as dist

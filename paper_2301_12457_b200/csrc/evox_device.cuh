@@ -185,9 +185,16 @@ template <> struct Fit<RASTRIGIN> {
 
 // Griewank: a_j = 1 - cos(x_j / sqrt(j+1)) = 2 sin^2(pi z), z = x_j h_j with
 // h_j = 1 / (2 pi sqrt(j+1)) (per-column constant: from the CTA's shared-memory
-// table when one exists, else computed with a correctly rounded rsqrt).
+// table when one exists (ld <= 4096), else computed per element: MUFU.RSQ plus one
+// Newton step, ~1 ulp -- the correctly rounded __frsqrt_rn cost 2.7x the kernel
+// time of evox_eval at dim 1e5; an h_j error of a few ulp moves f far below the
+// 1e-5 tolerance, and every kernel uses this same function, so fused and
+// standalone fitness stay bitwise equal).
 __device__ __forceinline__ float griewank_h(int64_t j) {
-    return __fmul_rn(0.15915494309189535f, __frsqrt_rn((float)(j + 1)));
+    const float x = (float)(j + 1);
+    const float y = rsqrtf(x);
+    const float r = __fmaf_rn(__fmul_rn(-0.5f * x, y), y, 1.5f);  // 1.5 - x y^2 / 2
+    return __fmul_rn(0.15915494309189535f, __fmul_rn(y, r));
 }
 
 template <> struct Fit<GRIEWANK> {

@@ -34,3 +34,22 @@ def test_bench_two_ranks_same_gpu(config):
     assert d["n_gpus"] == nproc and d["steps"] == 3 and d["value"] > 0
     assert d["roofline"]["bound"] == "hbm" and d["gpu_launches"] >= 3
     assert d["config"]["pop"] == 20000
+
+
+@pytest.mark.parametrize("config", ["EH-rosenbrock", "E5-griewank"])
+def test_bench_eval_line(config):
+    """SURVEY §8(d) evox_eval bench line: one JSON line, roofline against HBM, an e2e number
+    measured with host buffers (H2D of X and D2H of the fitness every step)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    cmd = [sys.executable, "bench.py", "--config", config, "--pop", "64", "--steps", "3",
+           "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "2"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["unit"] == "populations evaluated/s" and d["value"] > 0 and d["gpu_launches"] == 3
+    assert d["roofline"]["bound"] == "hbm" and d["roofline"]["frac"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 4 * 64 * ((d["config"]["dim"] + 3) // 4 * 4)
+    assert d["e2e"]["d2h_bytes_per_step"] == 4 * 64
