@@ -156,6 +156,15 @@ def cpu_baseline(cfg, target_s=12.0):
             "individual_dims_per_s": gens_per_s * cfg.pop * D * (0.5 if cfg.algo == "cso" else 1)}
 
 
+def _device_info(dev):
+    """device name, SM count, L2 size of the measuring GPU."""
+    import torch
+    p = torch.cuda.get_device_properties(dev)
+    return {"name": p.name, "sms": p.multi_processor_count,
+            "l2_mb": round(getattr(p, "L2_cache_size", 0) / 2**20, 1),
+            "hbm_gb": round(p.total_memory / 1e9, 1)}
+
+
 def _unit(cfg):
     return "populations evaluated/s" if cfg.algo == "eval" else "generations/s"
 
@@ -246,6 +255,7 @@ def run_eval(args, cfg, world, rank, local):
                          "kernel": f"k_eval<{cfg.problem}>", "kernel_ms": k_avg_ms,
                          "bytes_per_launch": bytes_launch, "peak_source": peak_src},
             "clocks": clk,
+            "device": _device_info(local),
             "gpu_launches": args.steps,
             "e2e": {"value": n_e2e / e2e_s, "unit": _unit(cfg),
                     "h2d_bytes_per_step": 4 * cfg.pop * ld, "d2h_bytes_per_step": 4 * cfg.pop,
@@ -515,6 +525,7 @@ def main():
                          "kernel_ms": k_avg_ms, "bytes_per_launch": bytes_launch,
                          "peak_source": peak_src},
             "clocks": clk,
+            "device": _device_info(local),
             # generation kernels timed by the library (+ the gbest select per step when W > 1)
             "gpu_launches": k_launch + (args.steps if (cfg.algo == "pso" and world > 1
                                                        and not peer) else 0),

@@ -200,47 +200,52 @@ __device__ __forceinline__ void walk_segment(Mover& mv, long long qb_, long long
     head_x = 0.0f;
     tail_valid = false;
     tail_x = 0.0f;
+    // one chunk: move (Mover::step), fitness terms, Rosenbrock halo -- in chunk order
+    auto chunk = [&](int u, int base) {
+        const int cb = base + G::LPR * u;  // first quad of this chunk
+        const int q = cb + sl;
+        const bool valid = row_ok && q < qe;
+        float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+            xn = mv.step(u, q);
+            fit_quad<P>(acc, xn, 4 * q, D, htab);
+        }
+        if constexpr (P == ROSENBROCK) {
+            const float nb = __shfl_down_sync(FULL, xn.x, 1, G::LPR);
+            const float f0 = __shfl_sync(FULL, xn.x, 0, G::LPR);
+            if (cb == qb) head_x = f0;
+            if (sl == G::LPR - 1 && pend) {
+                acc.pair(pend_x, f0);
+                pend = false;
+            }
+            if (valid) {
+                const bool has_next = 4 * q + 4 < D;
+                if (q + 1 < qe) {
+                    if (sl < G::LPR - 1) {
+                        if (has_next) acc.pair(xn.w, nb);
+                    } else {
+                        pend = has_next;
+                        pend_x = xn.w;
+                    }
+                } else {  // last quad of the segment: successor is the next segment's head
+                    tail_valid = has_next;
+                    tail_x = xn.w;
+                }
+            }
+        }
+    };
+    auto load = [&](int u, int base) {
+        const int q = base + G::LPR * u + sl;
+        if (row_ok && q < qe) mv.template load<G::EFL>(u, q);
+    };
     for (int base = qb; base < qe; base += G::GROUP) {
         pf(base);
 #pragma unroll
-        for (int u = 0; u < G::NU; ++u) {
-            const int q = base + G::LPR * u + sl;
-            if (row_ok && q < qe) mv.template load<G::EFL>(u, q);
-        }
+        for (int u = 0; u < G::NU; ++u) load(u, base);
 #pragma unroll
         for (int u = 0; u < G::NU; ++u) {
-            const int cb = base + G::LPR * u;  // first quad of this chunk
-            if (cb >= qe) break;                     // warp-uniform
-            const int q = cb + sl;
-            const bool valid = row_ok && q < qe;
-            float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid) {
-                xn = mv.step(u, q);
-                fit_quad<P>(acc, xn, 4 * q, D, htab);
-            }
-            if constexpr (P == ROSENBROCK) {
-                const float nb = __shfl_down_sync(FULL, xn.x, 1, G::LPR);
-                const float f0 = __shfl_sync(FULL, xn.x, 0, G::LPR);
-                if (cb == qb) head_x = f0;
-                if (sl == G::LPR - 1 && pend) {
-                    acc.pair(pend_x, f0);
-                    pend = false;
-                }
-                if (valid) {
-                    const bool has_next = 4 * q + 4 < D;
-                    if (q + 1 < qe) {
-                        if (sl < G::LPR - 1) {
-                            if (has_next) acc.pair(xn.w, nb);
-                        } else {
-                            pend = has_next;
-                            pend_x = xn.w;
-                        }
-                    } else {  // last quad of the segment: successor is the next segment's head
-                        tail_valid = has_next;
-                        tail_x = xn.w;
-                    }
-                }
-            }
+            if (base + G::LPR * u >= qe) break;  // warp-uniform
+            chunk(u, base);
         }
     }
 }
