@@ -76,6 +76,7 @@ cudaError_t launch_eval(int problem, const float* X, long long rows, long long D
     cudaGetDevice(&dev);
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
         const int g = grid_for((const void*)k_eval<P_, G_>, row_units<G_>(rows), dev);
+        carveout((const void*)k_eval<P_, G_>);
         k_eval<P_, G_><<<g, 256, 0, st>>>(X, rows, D, ld, fit);
     }));
     return cudaGetLastError();

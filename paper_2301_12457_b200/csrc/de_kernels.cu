@@ -264,6 +264,7 @@ int de_gen_grid(int problem, long long ld, long long rows, int device) {
 
 cudaError_t launch_de_gen(int problem, const DeArgs& a, int grid, cudaStream_t st) {
     EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+        carveout((const void*)k_de_gen<P_, G_, U_>);
         k_de_gen<P_, G_, U_><<<grid, 256, 0, st>>>(a);
     })));
     return cudaGetLastError();

@@ -27,6 +27,8 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_set>
 
 #include "evox_device.cuh"
 #include "evox_internal.h"
@@ -492,6 +494,21 @@ inline int grid_for(const void* fn, long long units, int device, int waves = 1) 
     return (int)(g < 1 ? 1 : g);
 }
 
+// EVOX_CARVE=c sets cudaFuncAttributePreferredSharedMemoryCarveout = c (percent of the
+// unified L1/shared array given to shared memory; 0 = largest L1) on the streaming kernels
+// once per kernel (tuning switch: in-flight LDG misses need L1 lines).
+inline void carveout(const void* fn) {
+    static const int c = [] {
+        const char* v = getenv("EVOX_CARVE");
+        return v && *v ? atoi(v) : -1;
+    }();
+    if (c < 0) return;
+    static std::mutex mu;
+    static std::unordered_set<const void*> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert(fn).second) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+}
+
 // Generation kernels are launched with programmatic stream serialization (PDL):
 // kernel t+1 becomes resident while kernel t retires (EVOX_NO_PDL=1: plain launch).
 template <class K, class A>
@@ -506,6 +523,7 @@ inline cudaError_t launch_pdl(K kernel, int grid, const A& a, cudaStream_t st, s
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = getenv("EVOX_NO_PDL") ? 0 : 1;
+    if (smem == 0) carveout((const void*)kernel);
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 

@@ -1,4 +1,4 @@
-// Microbenchmark: row-to-warp mapping and occupancy for the fused generation's access
+// Microbenchmark: row-to-warp mapping and occupancy (capped with dynamic smem) for the fused generation's access
 // pattern (3R2W: X V P read, X V written; 2R3W: X V read, X V P written), 1e6 x 1000 fp32,
 // warp per row, U = 4 float4 chunks in flight per lane, evict-first.  Occupancy is capped with
 // dynamic shared memory (the generation kernel runs 2 CTAs/SM at 128 registers).
@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(256) k_np(St s) {
 
 template <class K>
 void timeit(const char* name, int occ, K kern, int grid, St s, double bytes) {
-    const int smem = 0;
+    // cap residency at `occ` CTAs/SM with dynamic shared memory (228 KB per SM)
+    const int smem = occ >= 8 ? 0 : (220 * 1024) / occ - 2048;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -108,6 +109,11 @@ int main() {
         timeit("pers_2R3W", occ, k_pers<2, 3>, 148 * occ, s, b5);
         timeit("tick_2R3W", occ, k_tick<2, 3>, 148 * occ, s, b5);
     }
+    for (int occ : {2, 4}) {
+        timeit("np1_3R2W", occ, k_np<3, 2, 1>, npg1, s, b5);
+        timeit("np1_2R3W", occ, k_np<2, 3, 1>, npg1, s, b5);
+    }
+    timeit("pers_3R2W", 8, k_pers<3, 2>, 148 * 8, s, b5);
     timeit("np1_3R2W", 8, k_np<3, 2, 1>, npg1, s, b5);
     timeit("np4_3R2W", 8, k_np<3, 2, 4>, npg4, s, b5);
     timeit("np1_2R3W", 8, k_np<2, 3, 1>, npg1, s, b5);
