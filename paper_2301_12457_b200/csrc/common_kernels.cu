@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 
 #include "evox_device.cuh"
 #include "evox_internal.h"
@@ -17,11 +18,14 @@ namespace {
 template <int P, class G>
 __global__ void __launch_bounds__(256) k_eval(const float* __restrict__ X, long long rows,
                                               long long D, long long ld,
-                                              float* __restrict__ fit) {
+                                              float* __restrict__ fit,
+                                              const float* __restrict__ hg) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
-    __shared__ __align__(16) HStore<P> sh_h;
-    const float* htab = HTable<P, G>::fill(sh_h.v, ld);
+    __shared__ __align__(16) HStore<P, G> sh_h;
+    const float* htab;
+    if constexpr (P == GRIEWANK && G::WPR > 1) htab = hg;  // global table or nullptr
+    else htab = HTable<P, G>::fill(sh_h.v, ld);
     const RowMap<G> m(ld >> 2);
     NoPrefetch pf;
     for (long long it = 0;; ++it) {
@@ -38,6 +42,17 @@ __global__ void __launch_bounds__(256) k_eval(const float* __restrict__ X, long 
         const float f = reduce_row<P, G>(acc, D, hx, tx, tv, sh_acc, sh_head);
         if (m.leader && ok) fit[row] = f;
     }
+}
+
+// Griewank column constants for the CTA-per-row geometry (ld > HTAB): h[j] is
+// griewank_h(j) itself, so a kernel reading the table and one computing h_j per
+// element (the fused generations, or evox_eval under stream capture) produce the
+// same bits.  Saves the conversion + MUFU.RSQ + Newton step (~7 instructions of
+// ~30) per element for one L2-resident LDG.128 per quad.
+__global__ void k_griewank_table(float* __restrict__ h, long long n) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (long long)gridDim.x * blockDim.x)
+        h[j] = griewank_h(j);
 }
 
 // argmin key of a fitness vector (one CTA; for best() queries, not hot).
@@ -67,6 +82,40 @@ __global__ void k_debug_philox(const uint4* ctr, PhiloxKey rk, uint4* out, long 
 }
 
 
+// Per-device global table of griewank_h(j), j < cap, grown on demand (evox_eval
+// only).  Under stream capture (no allocation allowed) or on any allocation
+// failure, nullptr: the kernel then computes h_j per element, with the same bits.
+const float* griewank_table(long long ld, int dev, cudaStream_t st) {
+    static std::mutex mu;
+    static float* tab[64] = {};
+    static long long cap[64] = {};
+    if (dev < 0 || dev >= 64 || getenv("EVOX_NO_HTAB")) return nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+        return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cap[dev] < ld) {
+        if (tab[dev]) cudaFree(tab[dev]);  // synchronises the device: no reader in flight
+        tab[dev] = nullptr;
+        cap[dev] = 0;
+        float* p = nullptr;
+        if (cudaMalloc(&p, (size_t)ld * sizeof(float)) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        k_griewank_table<<<148, 256, 0, st>>>(p, ld);
+        if (cudaGetLastError() != cudaSuccess) {
+            cudaFree(p);
+            return nullptr;
+        }
+        // other streams may use the table next: make the fill complete first
+        if (cudaStreamSynchronize(st) != cudaSuccess) return nullptr;
+        tab[dev] = p;
+        cap[dev] = ld;
+    }
+    return tab[dev];
+}
+
 }  // namespace
 
 cudaError_t launch_eval(int problem, const float* X, long long rows, long long D, long long ld,
@@ -74,10 +123,12 @@ cudaError_t launch_eval(int problem, const float* X, long long rows, long long D
     if (rows <= 0) return cudaSuccess;
     int dev = 0;
     cudaGetDevice(&dev);
+    const float* hg = problem == GRIEWANK && geom_id(ld) == 2 ? griewank_table(ld, dev, st)
+                                                               : nullptr;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
         const int g = grid_for((const void*)k_eval<P_, G_>, row_units<G_>(rows), dev);
         carveout((const void*)k_eval<P_, G_>);
-        k_eval<P_, G_><<<g, 256, 0, st>>>(X, rows, D, ld, fit);
+        k_eval<P_, G_><<<g, 256, 0, st>>>(X, rows, D, ld, fit, hg);
     }));
     return cudaGetLastError();
 }

@@ -111,7 +111,7 @@ template <int P, class G, bool UNI>
 __global__ void __launch_bounds__(256, EVOX_MINB) k_de_gen(DeArgs a) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
-    __shared__ __align__(16) HStore<P> sh_h;
+    __shared__ __align__(16) HStore<P, G> sh_h;
     const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
     const RowMap<G> m(a.ld >> 2);
     const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;

@@ -229,7 +229,7 @@ template <int P, class G, bool UNI>
 __global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen(PsoArgs a) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
-    __shared__ __align__(16) HStore<P> sh_h;
+    __shared__ __align__(16) HStore<P, G> sh_h;
     const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
     const RowMap<G> m(a.ld >> 2);
     const int lane = lane_id();
@@ -317,7 +317,7 @@ template <int P, class G, bool UNI>
 __global__ void __launch_bounds__(256) k_pso_run_small(PsoArgs a, long long n_gens) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
-    __shared__ __align__(16) HStore<P> sh_h;
+    __shared__ __align__(16) HStore<P, G> sh_h;
     __shared__ unsigned long long sh_k[WARPS];
     __shared__ int sh_better;
     __shared__ long long sh_row;
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen_tma(PsoArgs a) {
     __shared__ __align__(8) uint64_t bars[WARPS][2];
     __shared__ Fit<P> sh_acc[1];
     __shared__ float sh_head[1];
-    __shared__ __align__(16) HStore<P> sh_h;
+    __shared__ __align__(16) HStore<P, G> sh_h;
     const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
     const RowMap<G> m(a.ld >> 2);
     const int lane = lane_id(), wid = threadIdx.x >> 5;

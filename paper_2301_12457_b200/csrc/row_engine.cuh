@@ -145,13 +145,16 @@ struct HTable<GRIEWANK, G> {
         }
     }
 };
-template <int P>
+// Shared-memory column table: only the warp-row geometries (ld <= HTAB) of
+// Griewank use it; the CTA-per-row geometry reads the global table of evox_eval
+// (or computes h_j per element) and must not give up 16 KB of L1 for nothing.
+template <int P, class G>
 struct HStore {
     float v[1];
 };
-template <>
-struct HStore<GRIEWANK> {
-    float v[HTAB];
+template <class G>
+struct HStore<GRIEWANK, G> {
+    float v[G::WPR > 1 ? 1 : HTAB];
 };
 
 // Programmatic dependent launch (PDL): a generation kernel lets the next one be

@@ -687,3 +687,15 @@ def test_fused_fitness_equals_evaluate(problem, N, D, monkeypatch):
     de.step(problem, 2)
     f = ev.evaluate(problem, de.view("X").clone(), dim=D).cpu().numpy()
     assert np.array_equal(f, de.view("F").cpu().numpy())
+
+
+@pytest.mark.parametrize("N,D", [(8, 4099), (3, 40001), (5, 100000)])
+def test_griewank_table_equals_per_element(N, D, monkeypatch):
+    """evox_eval's global Griewank column table (CTA-per-row geometry, ld > 4096) holds
+    griewank_h(j) itself: bitwise the per-element computation it replaces."""
+    X = torch.from_numpy(WL.padded(WL.uniform_rows(N, D, "griewank", seed=D))).cuda()
+    a = ev.evaluate("griewank", X, dim=D).cpu().numpy()
+    monkeypatch.setenv("EVOX_NO_HTAB", "1")
+    b = ev.evaluate("griewank", X, dim=D).cpu().numpy()
+    assert np.array_equal(a, b)
+    assert_fitness(a, O.evaluate("griewank", X.cpu().numpy()[:, :D]), f"griewank {N}x{D}")
