@@ -108,7 +108,7 @@ __device__ __forceinline__ void de_finalize(const DeArgs& a, unsigned long long 
 // One DE generation: trial of every target from the population at parity p,
 // evaluation, greedy "<=" replacement by flipping the buffer-select flag.
 template <int P, class G, bool UNI>
-__global__ void __launch_bounds__(256, EVOX_MINB) k_de_gen(DeArgs a) {
+__global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_DE_SHORT_MINB : EVOX_MINB) k_de_gen(DeArgs a) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
     __shared__ __align__(16) HStore<P, G> sh_h;

@@ -226,7 +226,7 @@ __global__ void k_pso_init(PsoArgs a) {
 
 // Fused PSO generation: lazy pbest + move + clip + evaluate + tell + argmin.
 template <int P, class G, bool UNI>
-__global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen(PsoArgs a) {
+__global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB : EVOX_MINB) k_pso_gen(PsoArgs a) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
     __shared__ __align__(16) HStore<P, G> sh_h;

@@ -43,6 +43,14 @@ namespace {
 #ifndef EVOX_MINB
 #define EVOX_MINB 2
 #endif
+// CTAs per SM the generation kernels are register-capped for in the short-row
+// (4 lanes/row, dim <= 128) geometry: tuning switches, measured in DESIGN.md §7
+#ifndef EVOX_PSO_SHORT_MINB
+#define EVOX_PSO_SHORT_MINB EVOX_MINB
+#endif
+#ifndef EVOX_DE_SHORT_MINB
+#define EVOX_DE_SHORT_MINB EVOX_MINB
+#endif
 #ifndef EVOX_AHEAD
 #define EVOX_AHEAD 4  // mode-B prefetch window, in lane groups
 #endif
@@ -239,6 +247,33 @@ __device__ __forceinline__ void walk_segment(Mover& mv, long long qb_, long long
             }
         }
     };
+    // Rosenbrock, interior group (every quad q of the group has q + 1 < qe and
+    // 4q + 4 < D): the same terms in the same order as `chunk`, without the
+    // per-element bounds and segment-end bookkeeping (E5-rosenbrock: ~23 -> ~10
+    // lane-instructions per element).  Bitwise equal to `chunk`.
+    auto chunk_interior = [&](int u, int base) {
+      if constexpr (P == ROSENBROCK) {
+        const int cb = base + G::LPR * u;
+        const int q = cb + sl;
+        float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row_ok) {
+            xn = mv.step(u, q);
+            acc.pair(xn.x, xn.y);
+            acc.pair(xn.y, xn.z);
+            acc.pair(xn.z, xn.w);
+        }
+        const float nb = __shfl_down_sync(FULL, xn.x, 1, G::LPR);
+        const float f0 = __shfl_sync(FULL, xn.x, 0, G::LPR);
+        if (cb == qb) head_x = f0;
+        if (sl == G::LPR - 1) {
+            if (pend) acc.pair(pend_x, f0);
+            pend = row_ok;
+            pend_x = xn.w;
+        } else if (row_ok) {
+            acc.pair(xn.w, nb);
+        }
+      }
+    };
     auto load = [&](int u, int base) {
         const int q = base + G::LPR * u + sl;
         if (row_ok && q < qe) mv.template load<G::EFL>(u, q);
@@ -247,6 +282,13 @@ __device__ __forceinline__ void walk_segment(Mover& mv, long long qb_, long long
         pf(base);
 #pragma unroll
         for (int u = 0; u < G::NU; ++u) load(u, base);
+        if constexpr (P == ROSENBROCK) {
+            if (base + G::GROUP < qe && 4LL * (base + G::GROUP) < D) {  // warp-uniform
+#pragma unroll
+                for (int u = 0; u < G::NU; ++u) chunk_interior(u, base);
+                continue;
+            }
+        }
 #pragma unroll
         for (int u = 0; u < G::NU; ++u) {
             if (base + G::LPR * u >= qe) break;  // warp-uniform
