@@ -41,6 +41,18 @@ def _env_int(k, d):
         return d
 
 
+def gen_kernel_name(cfg, rows, world):
+    """The generation kernel evox_*_step launches for this shard (mirrors the C-ABI's
+    dispatch: single-CTA persistent <= 2^16 elements, cooperative persistent <= 2^25 for
+    PSO at W = 1 unless EVOX_NO_MID is set, else one k_*_gen launch per generation)."""
+    n = rows * ((cfg.dim + 3) // 4 * 4)
+    if cfg.algo == "pso" and world == 1 and n <= 65536:
+        return f"k_pso_run_small<{cfg.problem}>"
+    if cfg.algo == "pso" and world == 1 and n <= (1 << 25) and not os.environ.get("EVOX_NO_MID"):
+        return f"k_pso_run_mid<{cfg.problem}>"
+    return f"k_{cfg.algo}_gen<{cfg.problem}>"
+
+
 def hbm_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -494,7 +506,9 @@ def main():
         peak, peak_src = hbm_peak()
         bytes_launch = algorithmic_bytes(cfg, rows)
         achieved = bytes_launch / (k_avg_ms * 1e-3) / 1e9
-        traffic = ncu_traffic(args.config)
+        kname = gen_kernel_name(cfg, rows, world)
+        # the committed ncu entry is per generation of the kernel that actually runs
+        traffic = ncu_traffic(args.config + ("-mid" if "run_mid" in kname else ""))
         gens_per_s = 1e3 / ms_per_step
         evaluated = cfg.pop * cfg.dim * (0.5 if cfg.algo == "cso" else 1.0)
         line = {
@@ -521,7 +535,7 @@ def main():
             "bytes_per_generation": algorithmic_bytes(cfg, cfg.pop),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": f"k_{cfg.algo}_gen<{cfg.problem}>",
+                         "kernel": kname,
                          "kernel_ms": k_avg_ms, "bytes_per_launch": bytes_launch,
                          "peak_source": peak_src},
             "clocks": clk,

@@ -673,6 +673,14 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
         s->t += n_gens;
         return EVOX_OK;
     }
+    // EVOX_NO_MID=1: per-generation launches at every size (testing / A-B timing)
+    const bool no_mid = std::getenv("EVOX_NO_MID") != nullptr;
+    if (!s->comm && !s->peer && !no_mid && !no_small && evox::pso_mid(s->rows, s->ld)) {
+        CU(s, timed(s, [&] { return evox::launch_pso_run_mid((int)problem, a, n_gens, s->stream); },
+                    n_gens));
+        s->t += n_gens;
+        return EVOX_OK;
+    }
     st = run_graphed(s, (int)problem, n_gens, [&]() -> evox_status {
         CU(s, timed(s, [&] { return evox::launch_pso_gen((int)problem, a, grid, s->stream); }));
         return pso_exchange(s);

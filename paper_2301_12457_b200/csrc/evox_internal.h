@@ -20,7 +20,7 @@ struct Ctl {
     unsigned int err;            // 1: peer exchange timed out (checked by the host at sync)
     unsigned long long t;        // index of the current population
     float gf;                    // best-so-far fitness (PSO) / scratch
-    int pad;                     // unused
+    unsigned int bar;            // k_pso_run_mid: grid barrier epoch (released per generation)
     long long gidx;              // global row of gbest (-1: none)
     float* hist;                 // hist[t] = min f of generation t
     unsigned long long* hkeys;   // CSO, world > 1: per-generation local min keys
@@ -135,6 +135,8 @@ int pso_gen_grid(int problem, long long ld, long long rows, int device);
 // Tiny populations: all generations in one single-CTA launch (bitwise identical).
 bool pso_small(long long rows, long long ld);
 cudaError_t launch_pso_run_small(int problem, const PsoArgs& a, long long n, cudaStream_t st);
+bool pso_mid(long long rows, long long ld);
+cudaError_t launch_pso_run_mid(int problem, const PsoArgs& a, long long n, cudaStream_t st);
 
 cudaError_t launch_cso_init(const CsoArgs& a, cudaStream_t st);
 cudaError_t launch_cso_tell0(const CsoArgs& a, cudaStream_t st);

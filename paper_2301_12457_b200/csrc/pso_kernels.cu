@@ -224,19 +224,14 @@ __global__ void k_pso_init(PsoArgs a) {
     }
 }
 
-// Fused PSO generation: lazy pbest + move + clip + evaluate + tell + argmin.
-template <int P, class G, bool UNI>
-__global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB : EVOX_MINB) k_pso_gen(PsoArgs a) {
-    __shared__ Fit<P> sh_acc[G::WPR];
-    __shared__ float sh_head[G::WPR];
-    __shared__ __align__(16) HStore<P, G> sh_h;
-    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
-    const RowMap<G> m(a.ld >> 2);
+// The rows of one fused PSO generation owned by this thread (lazy pbest + move +
+// clip + evaluate + tell); returns this thread's argmin key.  COH: G is re-read
+// through L2 (the persistent kernel rewrites it between generations).
+template <int P, class G, bool UNI, bool COH>
+__device__ __forceinline__ unsigned long long pso_gen_rows(const PsoArgs& a, const RowMap<G>& m,
+                                                           unsigned long long t, const float* htab,
+                                                           Fit<P>* sh_acc, float* sh_head) {
     const int lane = lane_id();
-    prefetch_first_rows<G>(a.X, a.V, a.rows, a.ld, m.wfirst, m.qb, m.qe);
-    pdl_wait();               // the previous generation (G, imp, pf, t) is complete
-    pdl_launch_dependents();  // the next generation may be scheduled as our CTAs retire
-    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
     const long long seg = m.qe - m.qb;
     // prefetch mode: A = the warp's whole next rows (short rows), B = sliding window
     const bool mode_a = seg * G::RPW <= MODE_A_MAX;
@@ -285,7 +280,7 @@ __global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB : EVOX_
         const bool pend_nn = nn < a.rows ? a.imp[nn] != 0 : true;
         float pf_old = 0.0f;
         if (m.leader && ok) pf_old = a.pf[row];
-        MoverPso<UNI> mv(a, ok ? row : 0, (uint32_t)t, pend_cur);
+        MoverPso<UNI, COH> mv(a, ok ? row : 0, (uint32_t)t, pend_cur);
         Fit<P> acc;
         float hx, tx;
         bool tv;
@@ -304,8 +299,76 @@ __global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB : EVOX_
         pend_nxt = pend_nn;
         wp.c = wp.c > seg ? wp.c - seg : 0;
     }
+    return best;
+}
+
+// Fused PSO generation: lazy pbest + move + clip + evaluate + tell + argmin.
+template <int P, class G, bool UNI>
+__global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB : EVOX_MINB) k_pso_gen(PsoArgs a) {
+    __shared__ Fit<P> sh_acc[G::WPR];
+    __shared__ float sh_head[G::WPR];
+    __shared__ __align__(16) HStore<P, G> sh_h;
+    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+    const RowMap<G> m(a.ld >> 2);
+    prefetch_first_rows<G>(a.X, a.V, a.rows, a.ld, m.wfirst, m.qb, m.qe);
+    pdl_wait();               // the previous generation (G, imp, pf, t) is complete
+    pdl_launch_dependents();  // the next generation may be scheduled as our CTAs retire
+    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
+    const unsigned long long best = pso_gen_rows<P, G, UNI, false>(a, m, t, htab, sh_acc, sh_head);
     unsigned long long key;
     if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
+}
+
+// Persistent PSO for mid-size populations (e.g. C2: 1e4 x 1000,
+// where a ~7 us per-launch fixed cost plus the launch gap is 20 % of a generation,
+// profiles/r01_c2_pop_sweep.txt): all n generations in ONE cooperative launch of
+// the resident grid, a grid-wide release/acquire barrier on ctl->bar between
+// generations instead of a kernel boundary.  Rows, reduction order and decisions
+// are those of k_pso_gen (same geometry, same per-row code), so the trajectory is
+// bitwise the stepwise one.  The barrier spin is bounded (ctl->err, no hang).
+template <int P, class G, bool UNI>
+__global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB : EVOX_MINB)
+    k_pso_run_mid(PsoArgs a, long long n) {
+    __shared__ Fit<P> sh_acc[G::WPR];
+    __shared__ float sh_head[G::WPR];
+    __shared__ __align__(16) HStore<P, G> sh_h;
+    __shared__ int sh_abort;
+    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+    const RowMap<G> m(a.ld >> 2);
+    Ctl* ctl = a.ctl;
+    // nobody writes ctl->bar before every CTA has arrived at the first grid_argmin,
+    // so every CTA reads the same base
+    const unsigned int base = *(volatile unsigned int*)&ctl->bar;
+    unsigned long long t = *(volatile unsigned long long*)&ctl->t;
+    for (long long g = 0; g < n; ++g, ++t) {
+        const unsigned long long best = pso_gen_rows<P, G, UNI, true>(a, m, t, htab, sh_acc, sh_head);
+        unsigned long long key;
+        const unsigned int target = base + (unsigned int)g + 1u;
+        if (grid_argmin(ctl, best, &key)) {
+            pso_finalize(a, key, t + 1);  // G, gf, gidx, hist; gen_key/ticket reset; t
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                st_release_gpu_u32(&ctl->bar, target);
+            }
+        } else if (g + 1 < n) {
+            if (threadIdx.x == 0) {
+                int abort = 0;
+                const unsigned long long t0 = globaltimer_ns();
+                while (ld_acquire_gpu_u32(&ctl->bar) != target) {
+                    if (globaltimer_ns() - t0 > 10000000000ull) {  // 10 s: not co-resident
+                        ctl->err = 1;
+                        abort = 1;
+                        break;
+                    }
+                    __nanosleep(64);
+                }
+                sh_abort = abort;
+            }
+            __syncthreads();
+            if (sh_abort) return;
+        }
+    }
 }
 
 
@@ -732,6 +795,26 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
 }
 
 bool pso_small(long long rows, long long ld) { return rows * ld <= 65536; }
+
+// Mid-size populations run n generations in one cooperative launch (k_pso_run_mid);
+// beyond ~2^25 elements a generation is long enough that the launch cost is noise.
+bool pso_mid(long long rows, long long ld) { return rows * ld <= (1LL << 25); }
+
+cudaError_t launch_pso_run_mid(int problem, const PsoArgs& a, long long n, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaSuccess;
+    EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+        const void* fn = (const void*)k_pso_run_mid<P_, G_, U_>;
+        carveout(fn);
+        const int grid = grid_for(fn, row_units<G_>(a.rows), dev);  // resident grid only
+        PsoArgs aa = a;
+        long long nn = n;
+        void* args[] = {&aa, &nn};
+        e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(256), args, 0, st);
+    })));
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
 
 cudaError_t launch_pso_run_small(int problem, const PsoArgs& a, long long n, cudaStream_t st) {
     EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {

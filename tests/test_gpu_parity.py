@@ -182,6 +182,29 @@ def test_pso_small_kernel_equals_grid_kernel(problem, N, D, lb, ub, seed, monkey
     assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
 
 
+@pytest.mark.parametrize("problem,N,D", [("ackley", 10_000, 1000),    # C2, warp per row
+                                         ("rosenbrock", 3001, 100),   # 4 lanes per row
+                                         ("griewank", 1999, 250),     # 8 lanes per row
+                                         ("rastrigin", 21, 5000),     # CTA per row
+                                         ("sphere", 700, 1001)])      # ragged tail
+def test_pso_mid_kernel_equals_stepwise(problem, N, D, monkeypatch):
+    """The persistent cooperative kernel (mid-size populations, n generations in one launch,
+    grid barrier between generations) is bitwise identical to one k_pso_gen launch per
+    generation; two step calls exercise the barrier epoch across launches."""
+    lb, ub = WL.BOUNDS[problem]
+    monkeypatch.delenv("EVOX_NO_MID", raising=False)
+    a = ev.PSO(N, D, lb, ub, seed=31)
+    a.step(problem, 10)
+    a.step(problem, 15)
+    monkeypatch.setenv("EVOX_NO_MID", "1")
+    b = ev.PSO(N, D, lb, ub, seed=31)
+    b.step(problem, 25)
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
+        assert np.array_equal(ga[k], gb[k]), k
+    assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
+
+
 @pytest.mark.parametrize("problem,N,D", [("ackley", 300, 1000), ("rosenbrock", 77, 1001),
                                          ("griewank", 64, 4096), ("rastrigin", 130, 600),
                                          ("sphere", 1000, 300)])
