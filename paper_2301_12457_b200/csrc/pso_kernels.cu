@@ -319,6 +319,10 @@ __global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB : EVOX_
     if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
 }
 
+#ifndef EVOX_MID_PF
+#define EVOX_MID_PF 1  // k_pso_run_mid: L2 prefetch of the next generation's first rows
+#endif
+
 // Persistent PSO for mid-size populations (e.g. C2: 1e4 x 1000,
 // where a ~7 us per-launch fixed cost plus the launch gap is 20 % of a generation,
 // profiles/r01_c2_pop_sweep.txt): all n generations in ONE cooperative launch of
@@ -342,6 +346,19 @@ __global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB : EVOX_
     unsigned long long t = *(volatile unsigned long long*)&ctl->t;
     for (long long g = 0; g < n; ++g, ++t) {
         const unsigned long long best = pso_gen_rows<P, G, UNI, true>(a, m, t, htab, sh_acc, sh_head);
+#if EVOX_MID_PF
+        // the warp's first rows of the next generation (its own, already final) go to L2
+        // while the grid drains the tail of this one (the pbest row only if not pending)
+        if (g + 1 < n && lane_id() == 0 && m.wfirst < a.rows) {
+            const long long nr = a.rows - m.wfirst < G::RPW ? a.rows - m.wfirst : G::RPW;
+            const long long o = m.wfirst * a.ld * 4 + m.qb * 16;
+            long long bytes = G::WPR == 1 ? nr * a.ld * 4 : (m.qe - m.qb) * 16;
+            if (bytes > 64 * 1024) bytes = 64 * 1024;
+            prefetch_l2(reinterpret_cast<const char*>(a.X) + o, bytes);
+            prefetch_l2(reinterpret_cast<const char*>(a.V) + o, bytes);
+            prefetch_l2(reinterpret_cast<const char*>(a.P) + o, bytes);
+        }
+#endif
         unsigned long long key;
         const unsigned int target = base + (unsigned int)g + 1u;
         if (grid_argmin(ctl, best, &key)) {
