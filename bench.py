@@ -48,7 +48,8 @@ def gen_kernel_name(cfg, rows, world):
     n = rows * ((cfg.dim + 3) // 4 * 4)
     if cfg.algo == "pso" and world == 1 and n <= 65536:
         return f"k_pso_run_small<{cfg.problem}>"
-    if cfg.algo == "pso" and world == 1 and n <= (1 << 25) and not os.environ.get("EVOX_NO_MID"):
+    cap = int(os.environ.get("EVOX_MID_MAX") or (1 << 25))
+    if cfg.algo == "pso" and world == 1 and n <= cap and not os.environ.get("EVOX_NO_MID"):
         return f"k_pso_run_mid<{cfg.problem}>"
     return f"k_{cfg.algo}_gen<{cfg.problem}>"
 

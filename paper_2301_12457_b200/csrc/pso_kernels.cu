@@ -46,9 +46,10 @@ struct MoverPso {
         const float4 xo = x[u];
         const float4 pb = pend ? xo : p[u];
         if (pend) st_stream(Pr + q, xo);
-        // G is read-only for a generation kernel (non-coherent path); the
-        // persistent small-population kernel rewrites it between generations.
-        const float4 g = G_COHERENT ? __ldcg(reinterpret_cast<const float4*>(a.G) + q)
+        // G is read-only for a generation kernel (non-coherent path); the persistent
+        // kernels rewrite it between generations: a plain (coherent, L1-cached) load,
+        // ordered after the rewrite by the barrier's acquire + bar.sync.
+        const float4 g = G_COHERENT ? *(reinterpret_cast<const float4*>(a.G) + q)
                                     : __ldg(reinterpret_cast<const float4*>(a.G) + q);
         const float4 lo = bound4t<UNI>(a.lb, a.lb0, q);
         const float4 hi = bound4t<UNI>(a.ub, a.ub0, q);
@@ -815,7 +816,13 @@ bool pso_small(long long rows, long long ld) { return rows * ld <= 65536; }
 
 // Mid-size populations run n generations in one cooperative launch (k_pso_run_mid);
 // beyond ~2^25 elements a generation is long enough that the launch cost is noise.
-bool pso_mid(long long rows, long long ld) { return rows * ld <= (1LL << 25); }
+bool pso_mid(long long rows, long long ld) {
+    static const long long cap = [] {  // EVOX_MID_MAX=elements: tuning switch
+        const char* v = getenv("EVOX_MID_MAX");
+        return v && *v ? atoll(v) : (1LL << 25);
+    }();
+    return rows * ld <= cap;
+}
 
 cudaError_t launch_pso_run_mid(int problem, const PsoArgs& a, long long n, cudaStream_t st) {
     int dev = 0;
