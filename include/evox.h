@@ -140,7 +140,11 @@ evox_status evox_pso_init(int64_t pop, int64_t dim, const float* lb, const float
  * n_gens fused generations [move -> evaluate -> tell] (+ the per-generation
  * gbest exchange when world > 1).  The problem is bound by the
  * first evaluation; a different problem later -> EVOX_ERR_CONTRACT.
- * n_gens >= 0.  Asynchronous (CUDA-graph replay). */
+ * n_gens >= 0.  Asynchronous (CUDA-graph replay of per-generation kernels; on
+ * one rank, populations of <= 2^16 elements run the n_gens in one single-CTA
+ * launch and <= 2^25 elements in one cooperative launch with a grid barrier
+ * per generation -- the same trajectory bitwise).  A barrier that times out
+ * (10 s) makes the next synchronising call return EVOX_ERR_EXCHANGE. */
 evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens);
 
 /* Unfused Algorithm.ask (Table I; Eq. (1)): the first ask on a fresh handle

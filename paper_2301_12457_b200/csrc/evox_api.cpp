@@ -280,7 +280,8 @@ evox_status sync_check(Base* b) {
         if (e != cudaSuccess) return poison(b, EVOX_ERR_CUDA, "reading the control block", e);
         if (err) {
             b->poisoned = true;
-            return fail(EVOX_ERR_EXCHANGE, "peer-memory exchange timed out waiting for a peer");
+            return fail(EVOX_ERR_EXCHANGE,
+                        "peer-memory exchange (or the persistent kernel's grid barrier) timed out");
         }
     }
     if (b->comm) {
