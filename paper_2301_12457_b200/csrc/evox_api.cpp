@@ -74,6 +74,8 @@ struct Base {
     std::map<std::pair<int, int64_t>, cudaGraphExec_t> graphs;
     unsigned long long* scratch_key = nullptr;  // one u64 for queries
     float* scratch_row = nullptr;               // [ld] for queries
+    unsigned char* stage = nullptr;             // pinned host staging of best() (Ctl + row)
+    size_t stage_bytes = 0;
     // kernel timing (evox_*_set_timing)
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
@@ -270,14 +272,20 @@ evox_status ensure_hist(Base* b, int64_t need) {
     return EVOX_OK;
 }
 
-evox_status sync_check(Base* b) {
+// staged: a host copy of the control block already enqueued on the stream (it is
+// complete after the synchronisation), so the error flag needs no extra copy.
+evox_status sync_check(Base* b, const Ctl* staged = nullptr) {
     DevGuard g(b->device);
     cudaError_t e = cudaStreamSynchronize(b->stream);
     if (e != cudaSuccess) return poison(b, EVOX_ERR_CUDA, "asynchronous CUDA error", e);
     if (b->ctl) {
         unsigned int err = 0;
-        e = cudaMemcpy(&err, &b->ctl->err, sizeof err, cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) return poison(b, EVOX_ERR_CUDA, "reading the control block", e);
+        if (staged) {
+            std::memcpy(&err, &staged->err, sizeof err);
+        } else {
+            e = cudaMemcpy(&err, &b->ctl->err, sizeof err, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) return poison(b, EVOX_ERR_CUDA, "reading the control block", e);
+        }
         if (err) {
             b->poisoned = true;
             return fail(EVOX_ERR_EXCHANGE,
@@ -315,6 +323,7 @@ void base_release(Base* b) {
     if (b->hkeys) cudaFree(b->hkeys);
     if (b->scratch_key) cudaFree(b->scratch_key);
     if (b->scratch_row) cudaFree(b->scratch_row);
+    if (b->stage) cudaFreeHost(b->stage);
     if (b->own_base && b->base) cudaFree(b->base);
     if (b->own_stream && b->stream) cudaStreamDestroy(b->stream);
     cudaGetLastError();
@@ -736,17 +745,34 @@ evox_status evox_pso_sync(evox_pso* s) {
     return sync_check(s);
 }
 
+// best() on a per-step path: the control block and the gbest row come back in ONE
+// stream-ordered copy pair into pinned staging and one synchronisation (instead of a
+// stream sync plus three blocking pageable copies), then the usual error checks.
 evox_status evox_pso_best(evox_pso* s, float* fit, int64_t* global_index, float* row_host) {
     evox_status st = check_pso(s);
     if (st != EVOX_OK) return st;
-    st = sync_check(s);
-    if (st != EVOX_OK) return st;
     DevGuard g(s->device);
+    const size_t row_bytes = sizeof(float) * (size_t)s->dim;
+    const size_t need = sizeof(Ctl) + row_bytes;
+    if (s->stage_bytes < need) {
+        if (s->stage) cudaFreeHost(s->stage);
+        s->stage = nullptr;
+        s->stage_bytes = 0;
+        CU(s, cudaHostAlloc((void**)&s->stage, need, cudaHostAllocDefault));
+        s->stage_bytes = need;
+    }
+    CU(s, cudaMemcpyAsync(s->stage, s->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s->stream));
+    if (row_host)
+        CU(s, cudaMemcpyAsync(s->stage + sizeof(Ctl), s->G, row_bytes, cudaMemcpyDeviceToHost,
+                              s->stream));
+    // stream sync + asynchronous-error / exchange-timeout checks (err from the staged copy)
+    st = sync_check(s, reinterpret_cast<const Ctl*>(s->stage));
+    if (st != EVOX_OK) return st;
     Ctl c;
-    CU(s, cudaMemcpy(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost));
+    std::memcpy(&c, s->stage, sizeof c);
     if (fit) *fit = c.gf;
     if (global_index) *global_index = c.gidx;
-    if (row_host) CU(s, cudaMemcpy(row_host, s->G, sizeof(float) * s->dim, cudaMemcpyDeviceToHost));
+    if (row_host) std::memcpy(row_host, s->stage + sizeof(Ctl), row_bytes);
     return EVOX_OK;
 }
 
