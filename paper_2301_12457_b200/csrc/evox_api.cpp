@@ -1843,7 +1843,6 @@ evox_status evox_de_best(evox_de* s, float* fit, int64_t* global_index, float* r
     DevGuard g(s->device);
     const int p = (int)((s->t < 0 ? 0 : s->t) & 1);
     if (!s->peer) CU(s, evox::launch_argmin_rows(s->f[p], s->rows, s->row0, s->scratch_key, s->stream));
-    if (row_host && !s->peer) CU(s, evox::launch_de_materialize(s->args(), s->stream));
     st = sync_check(s);
     if (st != EVOX_OK) return st;
     unsigned long long key = 0;
@@ -1865,8 +1864,12 @@ evox_status evox_de_best(evox_de* s, float* fit, int64_t* global_index, float* r
     if (fit) *fit = fv;
     if (global_index) *global_index = gi;
     if (row_host && gi >= 0) {
-        if (!s->peer) {
-            CU(s, cudaMemcpy(row_host, s->buf[0] + gi * s->ld, 4 * s->dim, cudaMemcpyDeviceToHost));
+        if (!s->peer) {  // the row's current buffer (no population-wide materialise)
+            const int64_t lr = gi - s->row0;
+            unsigned char sb = 0;
+            CU(s, cudaMemcpy(&sb, s->sel[p] + lr, 1, cudaMemcpyDeviceToHost));
+            CU(s, cudaMemcpy(row_host, s->buf[sb & 1] + lr * s->ld, 4 * s->dim,
+                             cudaMemcpyDeviceToHost));
         } else {  // the owner's current buffer, read through peer memory
             int w = 0;
             while (w + 1 < s->world && gi >= s->prow0[w + 1]) ++w;

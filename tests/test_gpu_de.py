@@ -96,6 +96,20 @@ def test_de_graphed_equals_stepwise_and_view_neutral():
     assert fa == a.view("F").cpu().numpy().min() and np.array_equal(ra, _state(a, D)[0][ia])
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("gens", [1, 2, 7])
+def test_de_best_row_before_any_gather(gens):
+    """best() reads the winning row from whichever of the two buffers holds it (no
+    population-wide gather): it must equal the row view("X") gathers afterwards."""
+    N, D, p = 300, 37, "rastrigin"
+    a = ev.DE(N, D, -5.12, 5.12, seed=11)
+    a.step(p, gens)
+    fa, ia, ra = a.best()
+    X = a.view("X").cpu().numpy()[:, :D]
+    F = a.view("F").cpu().numpy()
+    assert fa == F.min() and ia == int(np.argmin(F)) and np.array_equal(ra, X[ia])
+
+
 def test_de_large_population_sampled():
     """pop 2^20 x 100 (past the paper's 16,384 DE limit): one generation,
     sampled targets recomputed one by one by the oracle."""
