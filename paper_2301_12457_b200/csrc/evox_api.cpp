@@ -1322,6 +1322,10 @@ evox_status evox_cso_best(evox_cso* s, float* fit, int64_t* global_index, float*
         while (w + 1 < s->world && gi >= s->prow0[w + 1]) ++w;
         CU(s, cudaMemcpy(row_host, s->pX[w] + (gi - s->prow0[w]) * s->ld, 4 * s->dim,
                          cudaMemcpyDeviceToHost));
+    } else if (row_host && gi >= 0 && !api) {
+        // one rank: the stream is already synchronised and the row is local
+        CU(s, cudaMemcpy(row_host, s->X + (gi - s->row0) * s->ld, 4 * s->dim,
+                         cudaMemcpyDeviceToHost));
     } else if (row_host && gi >= 0) {
         const bool mine = gi >= s->row0 && gi < s->row0 + s->rows;
         if (mine)
