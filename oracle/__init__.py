@@ -70,6 +70,9 @@ def lib() -> ctypes.CDLL:
         L.oracle_argmin.restype = i64
         L.oracle_pso_run.argtypes = [i32, i64, i64, P, P, f32, f32, f32, u64, i64, i32, i32, i64,
                                      P, P, P, P, P, P, P, P, P, P, i32]
+        L.oracle_pso_tell.argtypes = [i64, i64, i32, P, P, P, P, P, P, P, P]
+        L.oracle_pso_run_with.argtypes = [i32, i64, i64, P, P, f32, f32, f32, i64, i32,
+                                          P, P, P, P, P, P, P, P, P, P, P, P]
         L.oracle_cso_perm.argtypes = [u32, u32, u32, u64, u64]
         L.oracle_cso_perm.restype = u32
         L.oracle_cso_loser_update_with.argtypes = [i64, P, P, P, P, P, P, f32, P, P, P]
@@ -171,6 +174,38 @@ def argmin(f) -> tuple[int, float]:
     m = np.zeros(1, np.float32)
     i = lib().oracle_argmin(f.shape[0], _p(f), _p(m))
     return int(i), float(m[0])
+
+
+def pso_tell(X, f, P, pf, G, gf, gidx, W=1):
+    """Unified tell of one generation (oracle_pso_tell), in place on P, pf, G.
+    Returns (gf, gidx, hist_t)."""
+    N, D = X.shape
+    gfa = np.array([gf], np.float32)
+    gia = np.array([gidx], np.int64)
+    h = np.zeros(1, np.float32)
+    lib().oracle_pso_tell(N, D, W, _p(_f32(X)), _p(_f32(f)), _p(P), _p(pf), _p(G), _p(gfa),
+                          _p(gia), _p(h))
+    return float(gfa[0]), int(gia[0]), float(h[0])
+
+
+def pso_run_with(problem, X, V, R1, R2, n_gens, w, phi_p, phi_g, lb, ub, W=1) -> PSOState:
+    """The stateful driver from a caller-supplied unevaluated (X, V) with injected r1/r2
+    (broadcast to [n_gens x N x D]); returns the state after n_gens generations."""
+    problem = PROBLEMS.get(problem, problem)
+    X = _f32(X).copy(); V = _f32(V).copy()
+    N, D = X.shape
+    lb, ub = _bounds(lb, ub, D)
+    R1 = _f32(np.broadcast_to(np.asarray(R1, np.float32), (max(n_gens, 1), N, D)))
+    R2 = _f32(np.broadcast_to(np.asarray(R2, np.float32), (max(n_gens, 1), N, D)))
+    P = np.zeros_like(X); pf = np.zeros(N, np.float32); f = np.zeros(N, np.float32)
+    F64 = np.zeros(N); G = np.zeros(D, np.float32)
+    gf = np.zeros(1, np.float32); gidx = np.zeros(1, np.int64)
+    hist = np.zeros(n_gens + 1, np.float32)
+    lib().oracle_pso_run_with(int(problem), N, D, _p(lb), _p(ub), w, phi_p, phi_g, n_gens, W,
+                              _p(X), _p(V), _p(P), _p(pf), _p(f), _p(F64), _p(G), _p(gf),
+                              _p(gidx), _p(hist), _p(R1), _p(R2))
+    return PSOState(int(problem), N, D, lb, ub, w, phi_p, phi_g, 0, X, V, P, pf, f, F64, G,
+                    float(gf[0]), int(gidx[0]), n_gens, [float(v) for v in hist])
 
 
 def cso_perm(x, B, blk, t, seed) -> int:

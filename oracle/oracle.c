@@ -252,18 +252,20 @@ int64_t oracle_argmin(int64_t rows, const float* f, float* fmin) {
     return best;
 }
 
-/* Evaluate + tell of one generation over W simulated shards (every
- * node evaluates its shard, the results are all-gathered, and one unified tell
- * follows; R-11 contiguous slices differing by <= 1). */
-static void eval_and_tell(int problem, int64_t N, int64_t D, int W, float* X, float* P,
-                          float* pf, float* f, double* F64, float* G, float* gf,
-                          int64_t* gidx, float* hist_t, int threads) {
+/* Tell of one generation over W simulated shards, given the generation's f32
+ * fitness (every node evaluates its shard, the results are
+ * all-gathered, and one unified tell follows; R-11 contiguous slices
+ * differing by <= 1).  Order (Listing 1, R-2): pbest
+ * first (S:316 strict, ties keep the incumbent), then each shard's winner
+ * (S:285 lowest index on ties), the shard winners combined by (fitness,
+ * global index) (S:349 first encountered on ties), and gbest moves only on a
+ * strict improvement over the incumbent (R-5). */
+void oracle_pso_tell(int64_t N, int64_t D, int W, const float* X, const float* f, float* P,
+                     float* pf, float* G, float* gf, int64_t* gidx, float* hist_t) {
     uint8_t* imp = (uint8_t*)malloc((size_t)(N > 0 ? N : 1));
     float best_f = INFINITY;
-    int64_t best_i = -1, r0 = 0, i;
+    int64_t best_i = -1, r0 = 0;
     int s;
-    oracle_eval(problem, N, D, X, F64, threads);
-    for (i = 0; i < N; ++i) f[i] = (float)F64[i];
     oracle_pso_tell_rows(N, D, X, f, P, pf, imp);
     for (s = 0; s < W; ++s) {
         int64_t rows = N / W + (s < N % W ? 1 : 0);
@@ -287,16 +289,33 @@ static void eval_and_tell(int problem, int64_t N, int64_t D, int W, float* X, fl
     free(imp);
 }
 
-/* Workflow.step (Listing 2; Eqs. (1)-(3) P:443-447), order R-2. */
-void oracle_pso_run(int problem, int64_t N, int64_t D, const float* lb, const float* ub,
-                    float w, float phi_p, float phi_g, uint64_t seed, int64_t n_gens,
-                    int W, int fresh, int64_t t0,
-                    float* X, float* V, float* P, float* pf, float* f, double* F64,
-                    float* G, float* gf, int64_t* gidx, float* hist, int threads) {
+/* Problem.evaluate (Eq. (2)) in fp64, rounded to f32 for every decision
+ * (R-9/R-10), then the unified tell. */
+static void eval_and_tell(int problem, int64_t N, int64_t D, int W, float* X, float* P,
+                          float* pf, float* f, double* F64, float* G, float* gf,
+                          int64_t* gidx, float* hist_t, int threads) {
+    int64_t i;
+    oracle_eval(problem, N, D, X, F64, threads);
+    for (i = 0; i < N; ++i) f[i] = (float)F64[i];
+    oracle_pso_tell(N, D, W, X, f, P, pf, G, gf, gidx, hist_t);
+}
+
+/* The stateful driver behind oracle_pso_run and oracle_pso_run_with:
+ * Workflow.step (Listing 2; Eqs. (1)-(3) P:443-447), order R-2:
+ * the state rests after evaluation; a fresh state is evaluated + told at t=0,
+ * then every generation is move(t) -> t+1 -> evaluate -> tell.
+ * mode 0: continue from generation t0; 1: fresh, X0/V0 from the seed (R-3);
+ * 2: fresh from the caller's X, V.  R1/R2 NULL: draw r1/r2 from Philox (tags
+ * 2, 3, R-6); else injected, dense [n_gens x N x D] (test hook). */
+static void pso_driver(int problem, int64_t N, int64_t D, const float* lb, const float* ub,
+                       float w, float phi_p, float phi_g, uint64_t seed, int64_t n_gens, int W,
+                       int mode, int64_t t0, float* X, float* V, float* P, float* pf, float* f,
+                       double* F64, float* G, float* gf, int64_t* gidx, float* hist,
+                       int threads, const float* R1, const float* R2) {
     int64_t g, t = t0, k = 0;
-    if (fresh) {
+    if (mode != 0) {
         int64_t i;
-        oracle_pso_init(N, D, 0, lb, ub, seed, X, V);
+        if (mode == 1) oracle_pso_init(N, D, 0, lb, ub, seed, X, V);
         memcpy(P, X, sizeof(float) * (size_t)(N * D));
         for (i = 0; i < N; ++i) pf[i] = INFINITY;
         *gf = INFINITY;
@@ -306,10 +325,33 @@ void oracle_pso_run(int problem, int64_t N, int64_t D, const float* lb, const fl
         eval_and_tell(problem, N, D, W, X, P, pf, f, F64, G, gf, gidx, &hist[k++], threads);
     }
     for (g = 0; g < n_gens; ++g) {
-        oracle_pso_move(N, D, 0, (uint64_t)t, seed, X, V, P, G, w, phi_p, phi_g, lb, ub, threads);
+        if (R1 == NULL)
+            oracle_pso_move(N, D, 0, (uint64_t)t, seed, X, V, P, G, w, phi_p, phi_g, lb, ub,
+                            threads);
+        else
+            oracle_pso_move_with(N, D, X, V, P, G, R1 + g * N * D, R2 + g * N * D, w, phi_p,
+                                 phi_g, lb, ub);
         t += 1;
         eval_and_tell(problem, N, D, W, X, P, pf, f, F64, G, gf, gidx, &hist[k++], threads);
     }
+}
+
+void oracle_pso_run(int problem, int64_t N, int64_t D, const float* lb, const float* ub,
+                    float w, float phi_p, float phi_g, uint64_t seed, int64_t n_gens,
+                    int W, int fresh, int64_t t0,
+                    float* X, float* V, float* P, float* pf, float* f, double* F64,
+                    float* G, float* gf, int64_t* gidx, float* hist, int threads) {
+    pso_driver(problem, N, D, lb, ub, w, phi_p, phi_g, seed, n_gens, W, fresh ? 1 : 0, t0, X, V,
+               P, pf, f, F64, G, gf, gidx, hist, threads, NULL, NULL);
+}
+
+void oracle_pso_run_with(int problem, int64_t N, int64_t D, const float* lb, const float* ub,
+                         float w, float phi_p, float phi_g, int64_t n_gens, int W,
+                         float* X, float* V, float* P, float* pf, float* f, double* F64,
+                         float* G, float* gf, int64_t* gidx, float* hist,
+                         const float* R1, const float* R2) {
+    pso_driver(problem, N, D, lb, ub, w, phi_p, phi_g, 0, n_gens, W, 2, 0, X, V, P, pf, f, F64,
+               G, gf, gidx, hist, 1, R1, R2);
 }
 
 /* ------------------------------------------------------------------- CSO */

@@ -64,6 +64,15 @@ void oracle_pso_tell_rows(int64_t rows, int64_t D, const float* X, const float* 
  * Returns the local index; *fmin gets f[i*] (NaN mapped to +inf). */
 int64_t oracle_argmin(int64_t rows, const float* f, float* fmin);
 
+/* Unified tell of one generation over W simulated shards (R-11),
+ * given the f32 fitness f [N] of X: pbest replacement (strict), each
+ * shard's argmin (lowest index on ties), shard winners combined by
+ * (fitness, global index), then gbest G [D] / *gf / *gidx move only
+ * on a strict improvement over the incumbent *gf (R-5).
+ * *hist_t = the generation's minimum f32 (NaN as +inf). */
+void oracle_pso_tell(int64_t N, int64_t D, int W, const float* X, const float* f, float* P,
+                     float* pf, float* G, float* gf, int64_t* gidx, float* hist_t);
+
 /* Whole PSO run, simulated-W mode (R-11): W contiguous row shards (sizes
  * differ by <= 1); every shard finds its local winner, then the winners are
  * combined by (fitness, global index) and gbest moves on strict improvement.
@@ -77,6 +86,16 @@ void oracle_pso_run(int problem, int64_t N, int64_t D, const float* lb, const fl
                     int W, int fresh, int64_t t0,
                     float* X, float* V, float* P, float* pf, float* f, double* F64,
                     float* G, float* gf, int64_t* gidx, float* hist, int threads);
+
+/* The same driver as oracle_pso_run, from a caller-supplied initial state X, V
+ * (not yet evaluated; P := X, pf = gf = +inf, gidx = -1, G = 0) and with
+ * injected r1 = R1, r2 = R2, dense [n_gens x N x D] (the test hook that
+ * replays the hand-worked trajectory through this driver).  hist [n_gens+1]. */
+void oracle_pso_run_with(int problem, int64_t N, int64_t D, const float* lb, const float* ub,
+                         float w, float phi_p, float phi_g, int64_t n_gens, int W,
+                         float* X, float* V, float* P, float* pf, float* f, double* F64,
+                         float* G, float* gf, int64_t* gidx, float* hist,
+                         const float* R1, const float* R2);
 
 /* CSO (Cheng & Jin, IEEE TCYB 2015; listed in Table II), R-8. */
 /* pi_{t,blk} on [0,B): 4-round Feistel on b=max(2,ceil(log2 B)) (even) bits,

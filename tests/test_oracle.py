@@ -191,6 +191,71 @@ def test_pso_hand_worked_two_particles(golden_dir):
     assert pf[1] == 1.25
 
 
+def test_pso_hand_worked_through_driver(golden_dir):
+    """The same golden trajectory replayed through the oracle's stateful C driver
+    (oracle_pso_run_with: the driver oracle_pso_run uses, with r1/r2 injected).  Pins the
+    driver's generation order evaluate -> tell (pbest, then gbest) -> move of Listing 1
+    P:243-277 / Eqs. (1)-(3) P:443-447 (R-2): any other order changes gen 1's fitness."""
+    g = _golden_pso(golden_dir)
+    for n in range(4):
+        s = O.pso_run_with("sphere", g["X0"], g["V0"], 0.5, 0.25, n, 0.5, 2.0, 1.0, -4.0, 4.0)
+        # hist[t] = min f32 of generation t (gens 0..n evaluated; golden f up to gen 2)
+        k = min(n + 1, 3)
+        assert len(s.hist) == n + 1
+        assert s.hist[:k] == [min(g[t][0]) for t in range(k)]
+        if n == 0:
+            assert np.array_equal(s.X, g["X0"]) and np.array_equal(s.V, g["V0"])
+            assert list(s.f) == g[0][0] and s.gidx == g[0][1]
+        else:
+            assert np.array_equal(s.X, g[n - 1][2]), (n, s.X)
+            assert np.array_equal(s.V, g[n - 1][3]), (n, s.V)
+            if n < 3:
+                assert list(s.f) == g[n][0] and s.gidx == g[n][1]
+    s = O.pso_run_with("sphere", g["X0"], g["V0"], 0.5, 0.25, 2, 0.5, 2.0, 1.0, -4.0, 4.0)
+    # after generation 2's tell: gbest = particle 0's X2 = (3/16, 27/32), f = 765/1024
+    assert s.gidx == 0 and s.gf == np.float32(765 / 1024)
+    assert np.array_equal(s.G, np.array([0.1875, 0.84375], np.float32))
+    assert np.array_equal(s.P[1], [-1.0, 0.5]) and s.pf[1] == 1.25
+    assert np.array_equal(s.P[0], s.G)
+
+
+def test_pso_tell_gbest_strict_against_incumbent():
+    """S:316 "strict improvement; ties keep incumbent" for gbest (SURVEY §8(c) argmin pin):
+    a generation whose minimum EQUALS the incumbent gf must not move G or gidx."""
+    X = np.array([[1.0, 1.0], [2.0, 2.0], [3.0, 3.0]], np.float32)
+    G = np.array([9.0, 9.0], np.float32)
+    P = X.copy(); pf = np.full(3, np.inf, np.float32)
+    gf, gidx, h = O.pso_tell(X, np.array([4.0, 2.0, 2.0], np.float32), P, pf, G, 2.0, 7)
+    assert (gf, gidx, h) == (2.0, 7, 2.0)
+    assert np.array_equal(G, [9.0, 9.0])
+    # a strictly better minimum moves it, to the lowest index among the tying rows
+    gf, gidx, h = O.pso_tell(X, np.array([4.0, 1.5, 1.5], np.float32), P, pf, G, 2.0, 7)
+    assert (gf, gidx, h) == (1.5, 1, 1.5)
+    assert np.array_equal(G, X[1])
+    # NaN ranks as +inf: an all-NaN generation never moves gbest, hist = +inf
+    gf, gidx, h = O.pso_tell(X, np.full(3, np.nan, np.float32), P, pf, G, 1.5, 1)
+    assert (gf, gidx) == (1.5, 1) and h == np.inf
+
+
+@pytest.mark.parametrize("W", [2, 3, 4])
+def test_pso_tell_shard_combine_ties_lowest_global_index(W):
+    """S:349 / S:285 / R-11: equal shard winners are combined to the LOWEST global index
+    (the first shard), whatever W; within a shard the lowest index wins too."""
+    N, D = 12, 3
+    X = np.arange(N * D, dtype=np.float32).reshape(N, D)
+    f = np.full(N, 5.0, np.float32)
+    bounds = np.cumsum([0] + [N // W + (s < N % W) for s in range(W)])
+    # plant the same minimum as the LAST row of every shard
+    for s in range(W):
+        f[bounds[s + 1] - 1] = 1.0
+    P = X.copy(); pf = np.full(N, np.inf, np.float32); G = np.zeros(D, np.float32)
+    gf, gidx, h = O.pso_tell(X, f, P, pf, G, np.inf, -1, W=W)
+    assert gidx == bounds[1] - 1 and gf == 1.0 and np.array_equal(G, X[gidx])
+    # and the same answer as W = 1 (sharding invariance, S:574)
+    P = X.copy(); pf = np.full(N, np.inf, np.float32); G1 = np.zeros(D, np.float32)
+    assert O.pso_tell(X, f, P, pf, G1, np.inf, -1, W=1)[1] == gidx
+
+
 def test_pso_clip_case():
     """R-4: positions clipped, velocity NOT clamped (SURVEY §8(c) clip case)."""
     X = np.array([[1.5]], np.float32); V = np.array([[1.0]], np.float32)
@@ -383,6 +448,60 @@ def test_cso_generation_invariants(N, B):
         assert f.min() <= f0.min()
         assert (X >= np.float32(-5.12)).all() and (X <= np.float32(5.12)).all()
         assert np.array_equal(f, O.evaluate("rastrigin", X).astype(np.float32))
+
+
+def test_cso_tie_goes_to_lower_global_index():
+    """R-8: equal fitness -> the LOWER global index wins and passes unchanged.  Every row
+    is a sign pattern of one vector a (Sphere f = sum a^2 for all rows, exactly), so every
+    pair is a tie: the higher index of each pair must be the (only) one that moves."""
+    rng = np.random.default_rng(21)
+    N, D, B, seed = 64, 9, 16, 5
+    a = rng.uniform(0.5, 2.0, D).astype(np.float32)
+    X = (a * rng.choice([-1.0, 1.0], (N, D))).astype(np.float32)
+    V = np.zeros_like(X)
+    F64 = O.evaluate("sphere", X); f = F64.astype(np.float32)
+    assert (f == f[0]).all()
+    X0 = X.copy()
+    O.cso_generation("sphere", X, V, f, F64, B, 3, seed, -5.12, 5.12)
+    for blk in range(N // B):
+        for p, q in O.cso_pairs(B, blk, 3, seed):
+            lo, hi = blk * B + min(p, q), blk * B + max(p, q)
+            assert np.array_equal(X[lo], X0[lo]), (lo, hi)
+            if not np.array_equal(X0[lo], X0[hi]):
+                assert not np.array_equal(X[hi], X0[hi]), (lo, hi)
+
+
+@pytest.mark.parametrize("B", [8, 32])
+def test_cso_xbar_is_the_column_mean(B):
+    """[CSO] Eq. (6) (R-8, R-15): xbar is the population MEAN position.  Closed forms:
+    (1) all rows equal -> xbar = that row, every difference is 0 and V0 = 0, so nothing
+    moves for any phi; (2) rows +-x in equal numbers -> xbar = 0 exactly, so each loser
+    follows the update with xbar = 0."""
+    N, D, seed = 32, 5, 3
+    row = np.array([1.5, -2.0, 0.25, 3.0, -0.5], np.float32)
+    X = np.tile(row, (N, 1)); V = np.zeros_like(X)
+    F64 = O.evaluate("sphere", X); f = F64.astype(np.float32)
+    O.cso_generation("sphere", X, V, f, F64, B, 0, seed, -5.12, 5.12, phi=0.3)
+    assert np.array_equal(X, np.tile(row, (N, 1))) and not V.any()
+    # (2) half +x, half -x: column mean 0
+    rng = np.random.default_rng(2)
+    H = rng.uniform(-4, 4, (N // 2, D)).astype(np.float32)
+    X = np.concatenate([H, -H]); X = X[rng.permutation(N)]
+    V = rng.uniform(-1, 1, (N, D)).astype(np.float32)
+    F64 = O.evaluate("sphere", X); f = F64.astype(np.float32)
+    X0, V0, f0 = X.copy(), V.copy(), f.copy()
+    t, phi = 4, 0.3
+    O.cso_generation("sphere", X, V, f, F64, B, t, seed, -5.12, 5.12, phi=phi)
+    for blk in range(N // B):
+        for p, q in O.cso_pairs(B, blk, t, seed):
+            i, k = blk * B + p, blk * B + q
+            w, l = (i, k) if (f0[i] < f0[k] or (f0[i] == f0[k] and i < k)) else (k, i)
+            R = [O.draw(1, D, l, t, tag, seed)[0] for tag in (5, 6, 7)]
+            xl, vl = X0[l].copy(), V0[l].copy()
+            O.cso_loser_update_with(X0[w], xl, vl, R[0], R[1], R[2], phi=phi,
+                                    xbar=np.zeros(D, np.float32), lb=-5.12, ub=5.12)
+            assert np.array_equal(X[l], xl) and np.array_equal(V[l], vl), (l, w)
+            assert np.array_equal(X[w], X0[w])
 
 
 # -------------------------------------------------------------------- DE
