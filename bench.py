@@ -44,12 +44,11 @@ def _env_int(k, d):
 def gen_kernel_name(cfg, rows, world):
     """The generation kernel evox_*_step launches for this shard (mirrors the C-ABI's
     dispatch: single-CTA persistent <= 2^16 elements, cooperative persistent <= 2^25 for
-    PSO at W = 1 unless EVOX_NO_MID is set, else one k_*_gen launch per generation)."""
+    PSO at W = 1, else one k_*_gen launch per generation)."""
     n = rows * ((cfg.dim + 3) // 4 * 4)
     if cfg.algo == "pso" and world == 1 and n <= 65536:
         return f"k_pso_run_small<{cfg.problem}>"
-    cap = int(os.environ.get("EVOX_MID_MAX") or (1 << 25))
-    if cfg.algo == "pso" and world == 1 and n <= cap and not os.environ.get("EVOX_NO_MID"):
+    if cfg.algo == "pso" and world == 1 and n <= (1 << 25):
         return f"k_pso_run_mid<{cfg.problem}>"
     return f"k_{cfg.algo}_gen<{cfg.problem}>"
 

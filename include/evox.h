@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define EVOX_ABI_VERSION 1
+#define EVOX_ABI_VERSION 2
 
 typedef enum {
     EVOX_OK = 0,
@@ -91,7 +91,22 @@ typedef struct {
     int device;              /* CUDA device ordinal; -1: the calling thread's current device */
     void* workspace;         /* optional device buffer for the state (see *_workspace_bytes) */
     size_t workspace_bytes;
+    uint32_t flags;          /* EVOX_FLAG_* bits; 0: the library picks every execution path */
+    int peer_timeout_ms;     /* peer-memory exchange wait limit (<= 0: 60 000 ms) */
 } evox_opts;
+
+/* evox_opts.flags.  They select among execution paths that are tested to give the SAME
+ * trajectory bitwise (same per-row reduction order, same decisions); they exist so tests
+ * can reach every path on one GPU.  No environment variable selects an execution path (the
+ * only one the library reads is EVOX_NCCL_LIB, a path to libnccl.so.2). */
+enum {
+    EVOX_FLAG_NO_SMALL = 1u << 0,   /* never run a step in the single-CTA persistent kernel */
+    EVOX_FLAG_NO_MID = 1u << 1,     /* never run a step in the cooperative persistent kernel */
+    EVOX_FLAG_TMA = 1u << 2,        /* PSO, 32 < ld/4 <= 1024: bulk-copy-staged generation kernel */
+    EVOX_FLAG_FORCE_NCCL = 1u << 3, /* world == 1: run the NCCL exchange path on a 1-rank
+                                       communicator (exercises the multi-GPU code) */
+    EVOX_FLAG_NO_GRAPH = 1u << 4    /* launch generations directly, not through CUDA graphs */
+};
 
 /* Description of the last failure on the calling thread ("" if none). */
 const char* evox_last_error(void);
@@ -119,6 +134,11 @@ evox_status evox_nccl_unique_id(uint8_t out[128]);
  * every init). */
 evox_status evox_eval(evox_problem problem, const float* X, int64_t pop, int64_t dim, int64_t ld,
                       float* fit, void* cuda_stream);
+/* evox_eval with flags: EVOX_EVAL_NO_HTAB computes the Griewank column constants per
+ * element instead of reading the per-device table (bitwise the same; test hook). */
+enum { EVOX_EVAL_NO_HTAB = 1u << 0 };
+evox_status evox_eval_ex(evox_problem problem, const float* X, int64_t pop, int64_t dim,
+                         int64_t ld, float* fit, void* cuda_stream, uint32_t flags);
 
 /* ---------------------------------------------------------------- PSO */
 /* Workspace bytes a handle of this shape needs (for evox_opts.workspace). */
@@ -219,7 +239,7 @@ evox_status evox_pso_kernel_time(evox_pso* s, double* total_ms, int64_t* gens, i
  *   (the mailboxes of all ranks, same process; GPUs must be peer-capable);
  *   mode 1 -- `peers` is world x 64 bytes of IPC handles (entry `rank` is
  *   ignored).  All ranks must connect before any of them steps.  A rank
- *   that waits more than 60 s (env EVOX_PEER_TIMEOUT_MS at connect time) for
+ *   that waits more than 60 s (evox_opts.peer_timeout_ms) for
  *   its peers stops waiting, flags the handle and the next synchronising
  *   call returns EVOX_ERR_EXCHANGE.  Single-
  *   process groups must not grow their history during a step (steps that

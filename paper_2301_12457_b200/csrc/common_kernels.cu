@@ -85,11 +85,11 @@ __global__ void k_debug_philox(const uint4* ctr, PhiloxKey rk, uint4* out, long 
 // Per-device global table of griewank_h(j), j < cap, grown on demand (evox_eval
 // only).  Under stream capture (no allocation allowed) or on any allocation
 // failure, nullptr: the kernel then computes h_j per element, with the same bits.
-const float* griewank_table(long long ld, int dev, cudaStream_t st) {
+const float* griewank_table(long long ld, int dev, cudaStream_t st, bool no_htab) {
     static std::mutex mu;
     static float* tab[64] = {};
     static long long cap[64] = {};
-    if (dev < 0 || dev >= 64 || getenv("EVOX_NO_HTAB")) return nullptr;
+    if (dev < 0 || dev >= 64 || no_htab) return nullptr;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
         return nullptr;
@@ -119,15 +119,14 @@ const float* griewank_table(long long ld, int dev, cudaStream_t st) {
 }  // namespace
 
 cudaError_t launch_eval(int problem, const float* X, long long rows, long long D, long long ld,
-                        float* fit, cudaStream_t st) {
+                        float* fit, cudaStream_t st, bool no_htab) {
     if (rows <= 0) return cudaSuccess;
     int dev = 0;
     cudaGetDevice(&dev);
-    const float* hg = problem == GRIEWANK && geom_id(ld) == 2 ? griewank_table(ld, dev, st)
+    const float* hg = problem == GRIEWANK && geom_id(ld) == 2 ? griewank_table(ld, dev, st, no_htab)
                                                                : nullptr;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
         const int g = grid_for((const void*)k_eval<P_, G_>, row_units<G_>(rows), dev);
-        carveout((const void*)k_eval<P_, G_>);
         k_eval<P_, G_><<<g, 256, 0, st>>>(X, rows, D, ld, fit, hg);
     }));
     return cudaGetLastError();

@@ -406,7 +406,6 @@ int cso_gen_grid(int problem, const CsoArgs& a, int device) {
 
 cudaError_t launch_cso_gen(int problem, const CsoArgs& a, int grid, cudaStream_t st) {
     EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM_ID(cso_geom_id(a.ld), {
-        carveout((const void*)k_cso_gen<P_, G_, U_>);
         k_cso_gen<P_, G_, U_><<<grid, 256, 0, st>>>(a);
     })));
     return cudaGetLastError();

@@ -234,8 +234,32 @@ __global__ void __launch_bounds__(256) k_de_materialize(DeArgs a) {
     }
 }
 
+// Gather the current population into `dst` WITHOUT touching buf/sel: with peers
+// connected, other ranks read this shard's rows through sel[p] in their generation
+// kernels, so the state must not change in place.
+__global__ void __launch_bounds__(256) k_de_gather(DeArgs a, float* __restrict__ dst) {
+    const int p = (int)(a.ctl->t & 1);
+    const long long NQ = a.ld >> 2;
+    const int wid = threadIdx.x >> 5, lane = lane_id();
+    for (long long row = (long long)blockIdx.x * WARPS + wid; row < a.rows;
+         row += (long long)gridDim.x * WARPS) {
+        const float* src = a.buf[a.sel[p][row] ? 1 : 0];
+        const float4* s = reinterpret_cast<const float4*>(src + row * a.ld);
+        float4* d = reinterpret_cast<float4*>(dst + row * a.ld);
+        for (long long q = lane; q < NQ; q += 32) d[q] = s[q];
+    }
+}
+
 
 }  // namespace
+
+cudaError_t launch_de_gather(const DeArgs& a, float* dst, cudaStream_t st) {
+    long long g = (a.rows + WARPS - 1) / WARPS;
+    if (g > 148 * 8) g = 148 * 8;
+    if (g < 1) g = 1;
+    k_de_gather<<<(int)g, 256, 0, st>>>(a, dst);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_de_init(const DeArgs& a, cudaStream_t st) {
     const long long total = a.rows * (a.ld >> 2);
@@ -264,7 +288,6 @@ int de_gen_grid(int problem, long long ld, long long rows, int device) {
 
 cudaError_t launch_de_gen(int problem, const DeArgs& a, int grid, cudaStream_t st) {
     EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-        carveout((const void*)k_de_gen<P_, G_, U_>);
         k_de_gen<P_, G_, U_><<<grid, 256, 0, st>>>(a);
     })));
     return cudaGetLastError();

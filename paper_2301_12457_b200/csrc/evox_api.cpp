@@ -56,6 +56,8 @@ struct Base {
     int64_t pop = 0, dim = 0, ld = 0, row0 = 0, rows = 0;
     int rank = 0, world = 1;
     uint64_t seed = 0;
+    uint32_t flags = 0;                                    // evox_opts.flags (EVOX_FLAG_*)
+    unsigned long long peer_timeout_ns = 60000000000ull;   // evox_opts.peer_timeout_ms
     std::vector<float> lb, ub;
     bool uniform = true;
     void* base = nullptr;
@@ -68,6 +70,7 @@ struct Base {
     unsigned long long* hkeys = nullptr;
     int64_t hist_cap = 0;
     int64_t t = -1;  // index of the current population (-1: not evaluated)
+    bool stepped = false;  // a step/ask ran since init or the last load (connect must precede)
     int problem = -1;
     bool poisoned = false;
     ncclComm_t comm = nullptr;
@@ -192,6 +195,11 @@ evox_status base_setup(Base* b, int64_t pop, int64_t dim, const float* lb, const
     b->world = world;
     b->rank = rank;
     b->seed = seed;
+    if (o) {
+        b->flags = o->flags;
+        if (o->peer_timeout_ms > 0)
+            b->peer_timeout_ns = (unsigned long long)o->peer_timeout_ms * 1000000ull;
+    }
     shard(pop, world, rank, &b->row0, &b->rows);
     b->lb.assign(b->ld, 0.0f);
     b->ub.assign(b->ld, 0.0f);
@@ -216,11 +224,11 @@ evox_status base_setup(Base* b, int64_t pop, int64_t dim, const float* lb, const
             return fail(EVOX_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
         b->own_stream = true;
     }
-    // EVOX_FORCE_NCCL=1 runs a single-GPU handle through the NCCL exchange path
+    // EVOX_FLAG_FORCE_NCCL runs a single-GPU handle through the NCCL exchange path
     // (a 1-rank communicator) so the multi-GPU code is exercised on one GPU.
-    const char* force = std::getenv("EVOX_FORCE_NCCL");
+    const bool force = (b->flags & EVOX_FLAG_FORCE_NCCL) != 0;
     // world > 1 without a unique id: the caller will evox_pso_connect() the peers
-    if ((world > 1 && o && o->nccl_id) || (world == 1 && force && *force == '1')) {
+    if ((world > 1 && o && o->nccl_id) || (world == 1 && force)) {
         const char* why = "";
         const evox::NcclApi* api = evox::nccl_api(&why);
         if (!api) return fail(EVOX_ERR_NCCL, "NCCL unavailable: %s", why);
@@ -393,7 +401,7 @@ constexpr int64_t kChunk = 32;
 
 template <class F>
 evox_status run_graphed(Base* b, int problem, int64_t n, F one) {
-    const bool no_graph = std::getenv("EVOX_NO_GRAPH") != nullptr;
+    const bool no_graph = (b->flags & EVOX_FLAG_NO_GRAPH) != 0;
     if (no_graph || b->timing) {
         for (int64_t i = 0; i < n; ++i) {
             evox_status st = one();
@@ -443,7 +451,6 @@ struct evox_pso : Base {
     size_t mb_bytes = 0;
     int64_t mb_slot = 0;
     bool peer = false;
-    unsigned long long peer_timeout_ns = 60ull * 1000 * 1000 * 1000;
     unsigned char* peers[evox::kMaxPeers] = {};
     std::vector<void*> ipc_opened;
     bool asked = false;   // ask issued, tell pending
@@ -455,6 +462,7 @@ struct evox_pso : Base {
         a.lb = lb_d; a.ub = ub_d;
         a.lb0 = lb[0]; a.ub0 = ub[0];
         a.uniform_bounds = uniform ? 1 : 0;
+        a.pf_next = evox::pso_prefetch_next(ld, rows) ? 1 : 0;
         a.rows = rows; a.row0 = row0; a.D = dim; a.ld = ld;
         a.w = w; a.phi_p = phi_p; a.phi_g = phi_g;
         a.cp = phi_p * 0x1p-24f;
@@ -557,8 +565,8 @@ evox_status evox_nccl_unique_id(uint8_t out[128]) {
     return EVOX_OK;
 }
 
-evox_status evox_eval(evox_problem problem, const float* X, int64_t pop, int64_t dim, int64_t ld,
-                      float* fit, void* cuda_stream) {
+evox_status evox_eval_ex(evox_problem problem, const float* X, int64_t pop, int64_t dim,
+                         int64_t ld, float* fit, void* cuda_stream, uint32_t flags) {
     if (!valid_problem(problem)) return fail(EVOX_ERR_INVALID_ARGUMENT, "unknown problem %d", (int)problem);
     if (pop < 0 || dim < 1) return fail(EVOX_ERR_SHAPE, "need pop >= 0 and dim >= 1");
     if (ld < dim || ld % 4) return fail(EVOX_ERR_SHAPE, "ld must be >= dim and a multiple of 4");
@@ -567,9 +575,15 @@ evox_status evox_eval(evox_problem problem, const float* X, int64_t pop, int64_t
     if (pop == 0) return EVOX_OK;
     if (!X || !fit) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL X or fit");
     if ((uintptr_t)X % 16) return fail(EVOX_ERR_INVALID_ARGUMENT, "X must be 16-byte aligned");
-    cudaError_t e = evox::launch_eval((int)problem, X, pop, dim, ld, fit, (cudaStream_t)cuda_stream);
+    cudaError_t e = evox::launch_eval((int)problem, X, pop, dim, ld, fit, (cudaStream_t)cuda_stream,
+                                      (flags & EVOX_EVAL_NO_HTAB) != 0);
     if (e != cudaSuccess) return fail(EVOX_ERR_CUDA, "evox_eval launch: %s", cudaGetErrorString(e));
     return EVOX_OK;
+}
+
+evox_status evox_eval(evox_problem problem, const float* X, int64_t pop, int64_t dim, int64_t ld,
+                      float* fit, void* cuda_stream) {
+    return evox_eval_ex(problem, X, pop, dim, ld, fit, cuda_stream, 0u);
 }
 
 evox_status evox_pso_workspace_bytes(int64_t pop, int64_t dim, int world, int rank, size_t* bytes) {
@@ -665,6 +679,7 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
         return fail(EVOX_ERR_CONTRACT, "handle is bound to problem %d (got %d)", s->problem, (int)problem);
     if (n_gens > (int64_t)0xFFFFFFFFll - 2 - s->t)
         return fail(EVOX_ERR_SHAPE, "generation counter would exceed 2^32");
+    s->stepped = true;
     DevGuard g(s->device);
     st = ensure_hist(s, (s->t < 0 ? 0 : s->t) + n_gens + 1);
     if (st != EVOX_OK) return st;
@@ -676,15 +691,15 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
     if (n_gens == 0) return EVOX_OK;
     const PsoArgs a = s->args();
     const int grid = s->gen_grid[problem];
-    const bool no_small = std::getenv("EVOX_NO_SMALL") != nullptr;  // testing: force multi-CTA
+    const bool no_small = (s->flags & EVOX_FLAG_NO_SMALL) != 0;  // testing: force multi-CTA
     if (!s->comm && !s->peer && !no_small && evox::pso_small(s->rows, s->ld)) {
         CU(s, timed(s, [&] { return evox::launch_pso_run_small((int)problem, a, n_gens, s->stream); },
                     n_gens));
         s->t += n_gens;
         return EVOX_OK;
     }
-    // EVOX_NO_MID=1: per-generation launches at every size (testing / A-B timing)
-    const bool no_mid = std::getenv("EVOX_NO_MID") != nullptr;
+    // EVOX_FLAG_NO_MID: per-generation launches at every size (testing / A-B timing)
+    const bool no_mid = (s->flags & EVOX_FLAG_NO_MID) != 0;
     if (!s->comm && !s->peer && !no_mid && !no_small && evox::pso_mid(s->rows, s->ld)) {
         CU(s, timed(s, [&] { return evox::launch_pso_run_mid((int)problem, a, n_gens, s->stream); },
                     n_gens));
@@ -692,7 +707,8 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
         return EVOX_OK;
     }
     st = run_graphed(s, (int)problem, n_gens, [&]() -> evox_status {
-        CU(s, timed(s, [&] { return evox::launch_pso_gen((int)problem, a, grid, s->stream); }));
+        CU(s, timed(s, [&] { return evox::launch_pso_gen((int)problem, a, grid, s->stream,
+                                                      (s->flags & EVOX_FLAG_TMA) != 0); }));
         return pso_exchange(s);
     });
     if (st != EVOX_OK) return st;
@@ -707,6 +723,7 @@ evox_status evox_pso_ask(evox_pso* s, const float** X_dev, int64_t* rows, int64_
     if (s->asked) return fail(EVOX_ERR_CONTRACT, "ask twice without tell");
     st = check_connected(s);
     if (st != EVOX_OK) return st;
+    s->stepped = true;
     DevGuard g(s->device);
     if (s->t < 0) {
         s->ask_t = 0;  // first ask: X0, unmoved
@@ -878,6 +895,9 @@ evox_status evox_pso_save(evox_pso* s, void* host_blob, size_t cap, size_t* used
 evox_status evox_pso_load(evox_pso* s, const void* host_blob, size_t size) {
     evox_status st = check_pso(s);
     if (st != EVOX_OK) return st;
+    if (s->peer)
+        return fail(EVOX_ERR_CONTRACT,
+                    "load on a peer-connected handle: load every rank's blob, then connect");
     if (!host_blob || size < sizeof(BlobHdr)) return fail(EVOX_ERR_INVALID_ARGUMENT, "bad blob");
     BlobHdr h;
     std::memcpy(&h, host_blob, sizeof h);
@@ -917,6 +937,8 @@ evox_status evox_pso_load(evox_pso* s, const void* host_blob, size_t size) {
     s->problem = (int)h.problem;
     s->asked = h.asked != 0;
     s->ask_t = h.ask_t;
+    s->stepped = false;
+    if (s->mbox) CU(s, cudaMemset(s->mbox, 0, s->mb_bytes));  // no stale exchange flags
     return EVOX_OK;
 }
 
@@ -948,7 +970,8 @@ evox_status evox_pso_connect(evox_pso* s, int mode, const void* peers) {
     if (!peers) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL peers");
     if (mode != 0 && mode != 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
     if (!s->mbox) return fail(EVOX_ERR_CONFIG, "peer exchange supports world <= %d", evox::kMaxPeers);
-    if (s->t >= 0 || s->asked) return fail(EVOX_ERR_CONTRACT, "connect before the first step/ask");
+    if (s->stepped || s->asked)
+        return fail(EVOX_ERR_CONTRACT, "connect before the first step/ask (after init or load)");
     DevGuard g(s->device);
     for (int r = 0; r < s->world; ++r) {
         if (r == s->rank) {
@@ -984,8 +1007,6 @@ evox_status evox_pso_connect(evox_pso* s, int mode, const void* peers) {
     // pre-size the history
     st = ensure_hist(s, 1 << 16);
     if (st != EVOX_OK) return st;
-    if (const char* ms = std::getenv("EVOX_PEER_TIMEOUT_MS"))  // tests shorten the 60 s default
-        s->peer_timeout_ns = (unsigned long long)std::strtoull(ms, nullptr, 10) * 1000000ull;
     s->peer = true;
     for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);  // args changed
     s->graphs.clear();
@@ -1041,7 +1062,6 @@ struct evox_cso : Base {
     bool aligned = true;  // every shard holds whole pairing blocks
     // global pairing across shards (evox_cso_connect)
     bool peer = false;
-    unsigned long long peer_timeout_ns = 60ull * 1000 * 1000 * 1000;
     float* pX[evox::kMaxPeers] = {};
     float* pf[evox::kMaxPeers][2] = {};
     unsigned char* pmbox[evox::kMaxPeers] = {};
@@ -1238,6 +1258,7 @@ evox_status evox_cso_step(evox_cso* s, evox_problem problem, int64_t n_gens) {
         return fail(EVOX_ERR_CONTRACT,
                     s->aligned ? "world > 1: pass opts.nccl_id at init or call evox_cso_connect"
                                : "pairing blocks straddle shards: call evox_cso_connect first");
+    s->stepped = true;
     DevGuard g(s->device);
     const int64_t t0 = s->t < 0 ? 0 : s->t;
     st = ensure_hist(s, t0 + n_gens + 1);
@@ -1290,6 +1311,11 @@ evox_status evox_cso_sync(evox_cso* s) {
 evox_status evox_cso_best(evox_cso* s, float* fit, int64_t* global_index, float* row_host) {
     evox_status st = check_cso(s);
     if (st != EVOX_OK) return st;
+    if (s->t < 0) {  // nothing evaluated yet: no best (the fitness arrays are unset)
+        if (fit) *fit = INFINITY;
+        if (global_index) *global_index = -1;
+        return sync_check(s);
+    }
     DevGuard g(s->device);
     const evox::NcclApi* api = (s->comm && !s->peer) ? evox::nccl_api(nullptr) : nullptr;
     if (!s->peer) {
@@ -1419,6 +1445,9 @@ evox_status evox_cso_save(evox_cso* s, void* host_blob, size_t cap, size_t* used
 evox_status evox_cso_load(evox_cso* s, const void* host_blob, size_t size) {
     evox_status st = check_cso(s);
     if (st != EVOX_OK) return st;
+    if (s->peer)
+        return fail(EVOX_ERR_CONTRACT,
+                    "load on a peer-connected handle: load every rank's blob, then connect");
     if (!host_blob || size < sizeof(BlobHdr)) return fail(EVOX_ERR_INVALID_ARGUMENT, "bad blob");
     BlobHdr h;
     std::memcpy(&h, host_blob, sizeof h);
@@ -1450,6 +1479,7 @@ evox_status evox_cso_load(evox_cso* s, const void* host_blob, size_t size) {
     CU(s, cudaMemcpy(s->ctl, &c, sizeof c, cudaMemcpyHostToDevice));
     s->t = h.t;
     s->problem = (int)h.problem;
+    s->stepped = false;
     return EVOX_OK;
 }
 
@@ -1473,7 +1503,7 @@ evox_status evox_cso_connect(evox_cso* s, int mode, const void* peers) {
     if (!peers) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL peers");
     if (mode != 0 && mode != 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
     if (s->world > evox::kMaxPeers) return fail(EVOX_ERR_CONFIG, "world <= %d", evox::kMaxPeers);
-    if (s->t >= 0) return fail(EVOX_ERR_CONTRACT, "connect before the first step");
+    if (s->stepped) return fail(EVOX_ERR_CONTRACT, "connect before the first step (after init or load)");
     DevGuard g(s->device);
     for (int r = 0; r < s->world; ++r) {
         unsigned char* base = nullptr;
@@ -1515,8 +1545,6 @@ evox_status evox_cso_connect(evox_cso* s, int mode, const void* peers) {
     }
     st = ensure_hist(s, 1 << 16);  // a step must never synchronise (single-process groups)
     if (st != EVOX_OK) return st;
-    if (const char* ms = std::getenv("EVOX_PEER_TIMEOUT_MS"))
-        s->peer_timeout_ns = (unsigned long long)std::strtoull(ms, nullptr, 10) * 1000000ull;
     s->peer = true;
     for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
     s->graphs.clear();
@@ -1573,12 +1601,12 @@ struct evox_de : Base {
     int gen_grid[5] = {0, 0, 0, 0, 0};
     // cross-shard donors (evox_de_connect)
     bool peer = false;
-    unsigned long long peer_timeout_ns = 60ull * 1000 * 1000 * 1000;
     float* pbuf[evox::kMaxPeers][2] = {};
     unsigned char* psel[evox::kMaxPeers][2] = {};
     unsigned char* pmbox[evox::kMaxPeers] = {};
     long long prow0[evox::kMaxPeers + 1] = {};
     std::vector<void*> ipc_opened;
+    float* gathered = nullptr;  // peers connected: view/save gather here, never in place
     evox::DeArgs args() const {
         evox::DeArgs a;
         std::memset(&a, 0, sizeof a);
@@ -1670,7 +1698,8 @@ evox_status evox_de_init(int64_t pop, int64_t dim, const float* lb, const float*
     if (pop > 0xFFFFFFFFll) return fail(EVOX_ERR_SHAPE, "pop must be < 2^32");
     if (round4(dim) > MAX_LD) return fail(EVOX_ERR_SHAPE, "dim must be <= 2^31 - 4 (in-row indices are 32-bit)");
     if (!mul_ok(pop, round4(dim), INT64_MAX / 64)) return fail(EVOX_ERR_SHAPE, "pop*dim overflows");
-    if (!std::isfinite(F)) return fail(EVOX_ERR_INVALID_ARGUMENT, "F must be finite");
+    if (!(F > 0.0f && F <= 2.0f))  // SPEC de_setup: F in (0, 2]
+        return fail(EVOX_ERR_INVALID_ARGUMENT, "F must be in (0, 2]");
     if (!(CR >= 0.0f && CR <= 1.0f)) return fail(EVOX_ERR_INVALID_ARGUMENT, "CR must be in [0,1]");
     evox_status st = check_bounds(dim, lb, ub);
     if (st != EVOX_OK) return st;
@@ -1725,6 +1754,7 @@ evox_status evox_de_step(evox_de* s, evox_problem problem, int64_t n_gens) {
         return fail(EVOX_ERR_SHAPE, "generation counter would exceed 2^32");
     if (s->world > 1 && !s->peer)
         return fail(EVOX_ERR_CONTRACT, "world > 1: call evox_de_connect before stepping");
+    s->stepped = true;
     DevGuard g(s->device);
     st = ensure_hist(s, (s->t < 0 ? 0 : s->t) + n_gens + 1);
     if (st != EVOX_OK) return st;
@@ -1746,6 +1776,27 @@ evox_status evox_de_step(evox_de* s, evox_problem problem, int64_t n_gens) {
     return EVOX_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// The current population as one [rows x ld] buffer.  Alone: materialise in place into
+// buf[0] (bitwise-neutral).  With peers connected: gather into a separate buffer, because
+// the peers' generation kernels read this shard's rows through buf/sel.
+evox_status de_current_population(evox_de* s, const float** X) {
+    if (!s->peer) {
+        CU(s, evox::launch_de_materialize(s->args(), s->stream));
+        *X = s->buf[0];
+        return EVOX_OK;
+    }
+    if (!s->gathered) CU(s, cudaMalloc(&s->gathered, sizeof(float) * (size_t)s->rows * s->ld));
+    CU(s, evox::launch_de_gather(s->args(), s->gathered, s->stream));
+    *X = s->gathered;
+    return EVOX_OK;
+}
+}  // namespace
+
+extern "C" {
+
 // Blob: header | X (gathered) | f (current parity) | hist[0..t]
 evox_status evox_de_save(evox_de* s, void* host_blob, size_t cap, size_t* used) {
     evox_status st = check_de(s);
@@ -1758,7 +1809,9 @@ evox_status evox_de_save(evox_de* s, void* host_blob, size_t cap, size_t* used) 
     if (!host_blob) return EVOX_OK;
     if (cap < need) return fail(EVOX_ERR_INVALID_ARGUMENT, "blob buffer too small");
     DevGuard g(s->device);
-    CU(s, evox::launch_de_materialize(s->args(), s->stream));
+    const float* X = nullptr;
+    st = de_current_population(s, &X);
+    if (st != EVOX_OK) return st;
     st = sync_check(s);
     if (st != EVOX_OK) return st;
     const int p = (int)((s->t < 0 ? 0 : s->t) & 1);
@@ -1771,7 +1824,7 @@ evox_status evox_de_save(evox_de* s, void* host_blob, size_t cap, size_t* used) 
     char* q = static_cast<char*>(host_blob);
     std::memcpy(q, &h, sizeof h);
     q += sizeof h;
-    CU(s, cudaMemcpy(q, s->buf[0], mat, cudaMemcpyDeviceToHost)); q += mat;
+    CU(s, cudaMemcpy(q, X, mat, cudaMemcpyDeviceToHost)); q += mat;
     CU(s, cudaMemcpy(q, s->f[p], 4 * s->rows, cudaMemcpyDeviceToHost)); q += 4 * s->rows;
     if (T > 0) CU(s, cudaMemcpy(q, s->hist, 4 * T, cudaMemcpyDeviceToHost));
     return EVOX_OK;
@@ -1780,6 +1833,9 @@ evox_status evox_de_save(evox_de* s, void* host_blob, size_t cap, size_t* used) 
 evox_status evox_de_load(evox_de* s, const void* host_blob, size_t size) {
     evox_status st = check_de(s);
     if (st != EVOX_OK) return st;
+    if (s->peer)
+        return fail(EVOX_ERR_CONTRACT,
+                    "load on a peer-connected handle: load every rank's blob, then connect");
     if (!host_blob || size < sizeof(BlobHdr)) return fail(EVOX_ERR_INVALID_ARGUMENT, "bad blob");
     BlobHdr h;
     std::memcpy(&h, host_blob, sizeof h);
@@ -1812,6 +1868,7 @@ evox_status evox_de_load(evox_de* s, const void* host_blob, size_t size) {
     CU(s, cudaMemcpy(s->ctl, &c, sizeof c, cudaMemcpyHostToDevice));
     s->t = h.t;
     s->problem = (int)h.problem;
+    s->stepped = false;
     return EVOX_OK;
 }
 
@@ -1829,10 +1886,13 @@ evox_status evox_de_view(evox_de* s, int field, void** dev, int64_t* rows, int64
     const int p = (int)((s->t < 0 ? 0 : s->t) & 1);
     int64_t r = s->rows, l = s->ld;
     switch (field) {
-        case EVOX_FIELD_X:
-            CU(s, evox::launch_de_materialize(s->args(), s->stream));
-            *dev = s->buf[0];
+        case EVOX_FIELD_X: {
+            const float* X = nullptr;
+            st = de_current_population(s, &X);
+            if (st != EVOX_OK) return st;
+            *dev = const_cast<float*>(X);
             break;
+        }
         case EVOX_FIELD_F: *dev = s->f[p]; l = 1; break;
         default: return fail(EVOX_ERR_INVALID_ARGUMENT, "field %d not available for DE", field);
     }
@@ -1844,6 +1904,11 @@ evox_status evox_de_view(evox_de* s, int field, void** dev, int64_t* rows, int64
 evox_status evox_de_best(evox_de* s, float* fit, int64_t* global_index, float* row_host) {
     evox_status st = check_de(s);
     if (st != EVOX_OK) return st;
+    if (s->t < 0) {  // nothing evaluated yet: no best (the fitness arrays are unset)
+        if (fit) *fit = INFINITY;
+        if (global_index) *global_index = -1;
+        return sync_check(s);
+    }
     DevGuard g(s->device);
     const int p = (int)((s->t < 0 ? 0 : s->t) & 1);
     if (!s->peer) CU(s, evox::launch_argmin_rows(s->f[p], s->rows, s->row0, s->scratch_key, s->stream));
@@ -1933,7 +1998,7 @@ evox_status evox_de_connect(evox_de* s, int mode, const void* peers) {
     if (st != EVOX_OK) return st;
     if (!peers) return fail(EVOX_ERR_INVALID_ARGUMENT, "NULL peers");
     if (mode != 0 && mode != 1) return fail(EVOX_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
-    if (s->t >= 0) return fail(EVOX_ERR_CONTRACT, "connect before the first step");
+    if (s->stepped) return fail(EVOX_ERR_CONTRACT, "connect before the first step (after init or load)");
     DevGuard g(s->device);
     for (int r = 0; r < s->world; ++r) {
         unsigned char* base = nullptr;
@@ -1975,8 +2040,6 @@ evox_status evox_de_connect(evox_de* s, int mode, const void* peers) {
     }
     st = ensure_hist(s, 1 << 16);  // a step must never synchronise (single-process groups)
     if (st != EVOX_OK) return st;
-    if (const char* ms = std::getenv("EVOX_PEER_TIMEOUT_MS"))
-        s->peer_timeout_ns = (unsigned long long)std::strtoull(ms, nullptr, 10) * 1000000ull;
     s->peer = true;
     for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
     s->graphs.clear();

@@ -41,6 +41,7 @@ struct PsoArgs {
     const float* ub;
     float lb0, ub0;
     int uniform_bounds;
+    int pf_next;          // 1: L2 bulk prefetch of the warp's next short rows (mode A)
     long long rows, row0, D, ld;
     float w, phi_p, phi_g;
     float cp, cg;         // phi_p * 2^-24, phi_g * 2^-24 (exact; see scaled_u24)
@@ -124,8 +125,12 @@ struct DeArgs {
 // ---- launchers (pso/cso/de/common_kernels.cu); all asynchronous on `st`.
 cudaError_t launch_pso_init(const PsoArgs& a, cudaStream_t st);
 cudaError_t launch_eval(int problem, const float* X, long long rows, long long D, long long ld,
-                        float* fit, cudaStream_t st);
-cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st);
+                        float* fit, cudaStream_t st, bool no_htab = false);
+// tma: the bulk-copy-staged variant (warp-per-row geometry only; EVOX_FLAG_TMA)
+cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st, bool tma);
+// Mode-A next-row L2 prefetch of the PSO generation (PsoArgs.pf_next): a schedule choice
+// measured per geometry and size, never a change of any result bit.
+bool pso_prefetch_next(long long ld, long long rows);
 cudaError_t launch_pso_move(const PsoArgs& a, unsigned long long t, cudaStream_t st);
 cudaError_t launch_pso_tell(const PsoArgs& a, const float* fit, unsigned long long t,
                             cudaStream_t st);
@@ -154,6 +159,7 @@ cudaError_t launch_de_tell0(const DeArgs& a, cudaStream_t st);
 int de_gen_grid(int problem, long long ld, long long rows, int device);
 cudaError_t launch_de_gen(int problem, const DeArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_de_materialize(const DeArgs& a, cudaStream_t st);
+cudaError_t launch_de_gather(const DeArgs& a, float* dst, cudaStream_t st);
 
 cudaError_t launch_debug_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out,
                                 long long n, cudaStream_t st);

@@ -49,12 +49,21 @@ struct MoverPso {
         // G is read-only for a generation kernel (non-coherent path); the persistent
         // kernels rewrite it between generations: a plain (coherent, L1-cached) load,
         // ordered after the rewrite by the barrier's acquire + bar.sync.
+#if EVOX_ABL & 4  // ablation (measurement builds only): no gbest load
+        const float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+#else
         const float4 g = G_COHERENT ? *(reinterpret_cast<const float4*>(a.G) + q)
                                     : __ldg(reinterpret_cast<const float4*>(a.G) + q);
+#endif
         const float4 lo = bound4t<UNI>(a.lb, a.lb0, q);
         const float4 hi = bound4t<UNI>(a.ub, a.ub0, q);
+#if EVOX_ABL & 1  // ablation: no Philox
+        const uint4 b1 = make_uint4(q * 0x9E3779B9u, row_g * 0x85EBCA6Bu, q ^ row_g, t);
+        const uint4 b2 = make_uint4(row_g * 0x9E3779B9u, q * 0x85EBCA6Bu, q + row_g, t);
+#else
         const uint4 b1 = Philox::run(make_uint4((uint32_t)q, row_g, t, 2u), a.rk);
         const uint4 b2 = Philox::run(make_uint4((uint32_t)q, row_g, t, 3u), a.rk);
+#endif
         float4 xn = xo, vn = v[u];
         const float w = a.w, cp = a.cp, cg = a.cg;
         pso_elem(xn.x, vn.x, pb.x, g.x, scaled_u24(b1.x, cp), scaled_u24(b2.x, cg), w, lo.x, hi.x);
@@ -259,7 +268,7 @@ __device__ __forceinline__ unsigned long long pso_gen_rows(const PsoArgs& a, con
         const bool ok = row < a.rows;
         const long long nxt = row + m.stride, nn = nxt + m.stride;
         const bool nxt_ok = nxt < a.rows;
-        if (mode_a && (EVOX_PF & 1)) {
+        if (mode_a && a.pf_next) {
             // the warp's next rows, HBM -> L2 now (X, V contiguous; P per row unless pending)
             const long long wn = wrow + m.stride;
             if (lane == 0 && wn < a.rows) {
@@ -305,7 +314,8 @@ __device__ __forceinline__ unsigned long long pso_gen_rows(const PsoArgs& a, con
 
 // Fused PSO generation: lazy pbest + move + clip + evaluate + tell + argmin.
 template <int P, class G, bool UNI>
-__global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB : EVOX_MINB) k_pso_gen(PsoArgs a) {
+__global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : (G::LPR == 4 ? EVOX_PSO_SHORT_MINB : EVOX_MINB))
+    k_pso_gen(PsoArgs a) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
     __shared__ __align__(16) HStore<P, G> sh_h;
@@ -776,30 +786,38 @@ cudaError_t launch_pso_init(const PsoArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Populations beyond the persistent cooperative kernel's range (> 2^25 elements).
+constexpr long long BIG = 1LL << 25;
+
+// Warp-per-row rows of a big population: no next-row L2 prefetch (it re-read 2.9 % of the
+// bytes and cost 4 points at H: 0.863 -> 0.900 without it) and 4 waves of resident CTAs
+// (+0.6 points); short rows (4 / 8 lanes per row) and L2-sized populations keep the
+// prefetch (C4g 0.764 vs 0.706 without; C2 0.678 vs 0.637), profiles/r02_pf.txt.
+bool pso_prefetch_next(long long ld, long long rows) {
+    return !(geom_id(ld) == 1 && rows * ld > BIG);
+}
+
 int pso_gen_grid(int problem, long long ld, long long rows, int device) {
+    const int waves = geom_id(ld) == 1 && rows * ld > BIG ? 4 : 1;
     int g = 1;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
-        g = grid_for((const void*)k_pso_gen<P_, G_, true>, row_units<G_>(rows), device);
+        g = grid_for((const void*)k_pso_gen<P_, G_, true>, row_units<G_>(rows), device, waves);
     }));
     return g;  // the TMA variant uses the same grid (2 CTAs/SM: 2 x 96 KB of staging)
 }
 
-// The TMA-staged kernel is an opt-in variant (EVOX_TMA=1) of the warp-per-row
-// geometry: measured 4-5 points BELOW the LDG + bulk-L2-prefetch kernel at H
-// and C2, so the LDG kernel is the default.
-static bool use_tma(long long ld) {
-    const char* v = getenv("EVOX_TMA");
-    return geom_id(ld) == 1 && U == 4 && v && *v == '1';
-}
+// The TMA-staged kernel is an opt-in variant (EVOX_FLAG_TMA) of the warp-per-row
+// geometry: measured 4-5 points BELOW the LDG kernel at H and C2.
+static bool use_tma(long long ld, bool tma) { return tma && geom_id(ld) == 1 && U == 4; }
 
 template <class K>
 static void tma_attr(K kernel) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
 }
 
-cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st, bool tma) {
     cudaError_t e = cudaSuccess;
-    if (use_tma(a.ld)) {
+    if (use_tma(a.ld, tma)) {
         EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, {
             tma_attr(k_pso_gen_tma<P_, U_>);
             e = launch_pdl(k_pso_gen_tma<P_, U_>, grid, a, st, TMA_SMEM);
@@ -815,14 +833,8 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
 bool pso_small(long long rows, long long ld) { return rows * ld <= 65536; }
 
 // Mid-size populations run n generations in one cooperative launch (k_pso_run_mid);
-// beyond ~2^25 elements a generation is long enough that the launch cost is noise.
-bool pso_mid(long long rows, long long ld) {
-    static const long long cap = [] {  // EVOX_MID_MAX=elements: tuning switch
-        const char* v = getenv("EVOX_MID_MAX");
-        return v && *v ? atoll(v) : (1LL << 25);
-    }();
-    return rows * ld <= cap;
-}
+// beyond 2^25 elements a generation is long enough that the launch cost is noise.
+bool pso_mid(long long rows, long long ld) { return rows * ld <= BIG; }
 
 cudaError_t launch_pso_run_mid(int problem, const PsoArgs& a, long long n, cudaStream_t st) {
     int dev = 0;
@@ -830,7 +842,6 @@ cudaError_t launch_pso_run_mid(int problem, const PsoArgs& a, long long n, cudaS
     cudaError_t e = cudaSuccess;
     EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
         const void* fn = (const void*)k_pso_run_mid<P_, G_, U_>;
-        carveout(fn);
         const int grid = grid_for(fn, row_units<G_>(a.rows), dev);  // resident grid only
         PsoArgs aa = a;
         long long nn = n;

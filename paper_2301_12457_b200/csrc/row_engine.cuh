@@ -27,8 +27,6 @@
 
 #include <cstdint>
 #include <cstdlib>
-#include <mutex>
-#include <unordered_set>
 
 #include "evox_device.cuh"
 #include "evox_internal.h"
@@ -39,6 +37,9 @@ namespace {
 
 #ifndef EVOX_U
 #define EVOX_U 4
+#endif
+#ifndef EVOX_ABL
+#define EVOX_ABL 0  // ablation bits for measurement builds only; 0 in the product
 #endif
 #ifndef EVOX_MINB
 #define EVOX_MINB 2
@@ -51,12 +52,15 @@ namespace {
 #ifndef EVOX_DE_SHORT_MINB
 #define EVOX_DE_SHORT_MINB EVOX_MINB
 #endif
+#ifndef EVOX_ROW_MINB
+#define EVOX_ROW_MINB 3  // CTA-per-row geometry (ld > 4096): C5 0.872 -> 0.909 (r02_pf.txt)
+#endif
 #ifndef EVOX_AHEAD
 #define EVOX_AHEAD 4  // mode-B prefetch window, in lane groups
 #endif
 #ifndef EVOX_PF
-// L2 bulk-prefetch switches (measured): bit 0 mode A (a warp's next short
-// rows: +2-4 points at dim <= 1000; on), bit 1 mode B (sliding window inside long rows:
+// L2 bulk-prefetch switches (measured): bit 0 unused (mode A, a warp's next
+// short rows, is the runtime PsoArgs.pf_next: pso_prefetch_next), bit 1 mode B (sliding window inside long rows:
 // -13 points at dim 1e5; off), bit 2 CSO winner/loser rows of the next item (neutral; off),
 // bit 3 the first rows of a PDL-launched generation (neutral; off).
 #define EVOX_PF 1
@@ -221,7 +225,10 @@ __device__ __forceinline__ void walk_segment(Mover& mv, long long qb_, long long
         float4 xn = make_float4(0.f, 0.f, 0.f, 0.f);
         if (valid) {
             xn = mv.step(u, q);
+#if EVOX_ABL & 2  // ablation (measurement builds only): no fitness terms
+#else
             fit_quad<P>(acc, xn, 4 * q, D, htab);
+#endif
         }
         if constexpr (P == ROSENBROCK) {
             const float nb = __shfl_down_sync(FULL, xn.x, 1, G::LPR);
@@ -509,14 +516,9 @@ using GW8 = Geom<32, 8, 3>;  // long rows: 3 chunks in flight measured best (C5)
 // 3: 4 lanes per row (ld <= 128), 0: 8 lanes per row (ld <= 256), 1: a warp per
 // row (ld <= 4096), 2: a CTA per row.  Narrow row groups keep short rows from
 // idling lanes (dim 100 = 25 quads: 28 lane-slots with 4 lanes vs 32 with 8).
+// A function of ld only: every reduction order -- hence every fitness bit -- is fixed by
+// the dimension, whatever the population, shard count or launch grid (R-11).
 inline int geom_id(long long ld) {
-    // EVOX_GEOM=id forces one geometry for every launch of the process (tuning sweeps only:
-    // results stay exact, but reduction orders -- hence fitness bits -- follow the geometry)
-    static const int forced = [] {
-        const char* g = getenv("EVOX_GEOM");
-        return g && *g ? atoi(g) : -1;
-    }();
-    if (forced >= 0 && forced <= 3) return forced;
     const long long NQ = ld >> 2;
     if (NQ <= 32) return 3;
     if (NQ <= 64) return 0;
@@ -524,47 +526,27 @@ inline int geom_id(long long ld) {
     return 2;
 }
 
-// `waves` x (resident CTAs): 1 = persistent grid-stride (PSO, CSO: measured best); the DE
-// generation takes 16 (pop 1e6 x dim 100: +14 %, neutral at dim 1000).
 // CSO generation: 8 lanes per row up to 1024 quads (one warp walks 4 independent pairs at
 // once, so more scattered winner/loser rows are in flight: C3 71 -> 77 % of HBM peak; PSO
 // and DE measured worse with it). Still a function of ld only (R-11).
 inline int cso_geom_id(long long ld) {
     const int g = geom_id(ld);
-    return g == 1 && getenv("EVOX_GEOM") == nullptr ? 0 : g;
+    return g == 1 ? 0 : g;
 }
 
+// `waves` x (resident CTAs), at most one CTA per row unit.  The grid never changes a result
+// bit (every reduction is per row; the argmin is exact), only the schedule.
 inline int grid_for(const void* fn, long long units, int device, int waves = 1) {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
     if (per_sm < 1) per_sm = 1;
     long long g = (long long)sm_count(device) * per_sm * waves;
-    // EVOX_NP=k: k waves of resident CTAs (k = 0: one CTA per row unit)
-    if (const char* np = getenv("EVOX_NP")) {
-        const long long k = atoll(np);
-        g = k <= 0 ? units : (long long)sm_count(device) * per_sm * k;
-    }
     if (units < g) g = units;
     return (int)(g < 1 ? 1 : g);
 }
 
-// EVOX_CARVE=c sets cudaFuncAttributePreferredSharedMemoryCarveout = c (percent of the
-// unified L1/shared array given to shared memory; 0 = largest L1) on the streaming kernels
-// once per kernel (tuning switch: in-flight LDG misses need L1 lines).
-inline void carveout(const void* fn) {
-    static const int c = [] {
-        const char* v = getenv("EVOX_CARVE");
-        return v && *v ? atoi(v) : -1;
-    }();
-    if (c < 0) return;
-    static std::mutex mu;
-    static std::unordered_set<const void*> done;
-    std::lock_guard<std::mutex> lk(mu);
-    if (done.insert(fn).second) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-}
-
 // Generation kernels are launched with programmatic stream serialization (PDL):
-// kernel t+1 becomes resident while kernel t retires (EVOX_NO_PDL=1: plain launch).
+// kernel t+1 becomes resident while kernel t retires.
 template <class K, class A>
 inline cudaError_t launch_pdl(K kernel, int grid, const A& a, cudaStream_t st, size_t smem = 0) {
     cudaLaunchConfig_t cfg = {};
@@ -576,8 +558,7 @@ inline cudaError_t launch_pdl(K kernel, int grid, const A& a, cudaStream_t st, s
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = getenv("EVOX_NO_PDL") ? 0 : 1;
-    if (smem == 0) carveout((const void*)kernel);
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 

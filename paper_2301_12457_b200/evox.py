@@ -18,7 +18,8 @@ from typing import Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-# EVOX_LIB selects a tuning variant built by _build.build(defines=...) (in-tree)
+# The product library.  EVOX_LIB (measurement scripts only: ablation / tuning builds under
+# variants/, never the default) overrides it; bench.py reports the path it loaded.
 LIB_PATH = os.environ.get("EVOX_LIB") or os.path.join(_PKG, "libevox.so")
 
 PROBLEMS = {"sphere": 0, "ackley": 1, "rastrigin": 2, "griewank": 3, "rosenbrock": 4}
@@ -56,7 +57,15 @@ _EXC = {INVALID_ARGUMENT: InvalidArgument, SHAPE: ShapeError, CONTRACT: Contract
 class EvoxOpts(ctypes.Structure):
     _fields_ = [("cuda_stream", ctypes.c_void_p), ("nccl_id", ctypes.c_void_p),
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("device", ctypes.c_int),
-                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+                ("flags", ctypes.c_uint32), ("peer_timeout_ms", ctypes.c_int)]
+
+
+# evox_opts.flags (include/evox.h): execution-path selectors that never change a result bit
+FLAG_NO_SMALL, FLAG_NO_MID, FLAG_TMA, FLAG_FORCE_NCCL, FLAG_NO_GRAPH = 1, 2, 4, 8, 16
+EVAL_NO_HTAB = 1
+# peer-memory exchange wait limit for new handles (0: the library default, 60 s)
+DEFAULT_PEER_TIMEOUT_MS = 0
 
 
 # Exported symbols and their signatures (restype evox_status unless noted).
@@ -73,6 +82,7 @@ SIGNATURES = {
     "evox_shard_rows": ([_i64, _i, _i, _PI64, _PI64], _i),
     "evox_nccl_unique_id": ([_p], _i),
     "evox_eval": ([_i, _p, _i64, _i64, _i64, _p, _p], _i),
+    "evox_eval_ex": ([_i, _p, _i64, _i64, _i64, _p, _p, _u32], _i),
     "evox_pso_workspace_bytes": ([_i64, _i64, _i, _i, _PSZ], _i),
     "evox_pso_init": ([_i64, _i64, _p, _p, _f32, _f32, _f32, _u64, _p, _PP], _i),
     "evox_pso_step": ([_p, _i, _i64], _i),
@@ -200,7 +210,7 @@ def _stream_ptr(stream) -> Optional[int]:
     return int(stream.cuda_stream)
 
 
-def evaluate(problem, X, dim: Optional[int] = None, out=None, stream=None):
+def evaluate(problem, X, dim: Optional[int] = None, out=None, stream=None, flags: int = 0):
     """Problem.evaluate (Eq. (2)): fitness of every row of the CUDA float32 tensor X.
 
     X is [pop, ld] with ld % 4 == 0 (``dim`` <= ld columns are used; default
@@ -216,8 +226,8 @@ def evaluate(problem, X, dim: Optional[int] = None, out=None, stream=None):
         out = torch.empty(pop, dtype=torch.float32, device=X.device)
     if stream is None:
         stream = torch.cuda.current_stream(X.device)
-    _check(lib().evox_eval(problem_id(problem), X.data_ptr(), pop, dim, ld, out.data_ptr(),
-                           _stream_ptr(stream)))
+    _check(lib().evox_eval_ex(problem_id(problem), X.data_ptr(), pop, dim, ld, out.data_ptr(),
+                              _stream_ptr(stream), int(flags)))
     return out
 
 
@@ -246,8 +256,10 @@ def _device_of(device) -> int:
     return torch.cuda.current_device()
 
 
-def _opts(stream, rank, world, device, nccl_id, workspace):
+def _opts(stream, rank, world, device, nccl_id, workspace, flags=0, peer_timeout_ms=None):
     o = EvoxOpts()
+    o.flags = int(flags)
+    o.peer_timeout_ms = int(DEFAULT_PEER_TIMEOUT_MS if peer_timeout_ms is None else peer_timeout_ms)
     o.cuda_stream = _stream_ptr(stream)
     o.rank = rank
     o.world = world
@@ -363,11 +375,13 @@ class PSO(_Handle):
     def __init__(self, pop: int, dim: int, lb=-5.12, ub=5.12, w: float = 0.6,
                  phi_p: float = 2.5, phi_g: float = 0.8, seed: int = 0, stream=None,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
-                 device: Optional[int] = None, workspace=None):
+                 device: Optional[int] = None, workspace=None, flags: int = 0,
+                 peer_timeout_ms: Optional[int] = None):
         self._h = None
         self.pop, self.dim = int(pop), int(dim)
         lbv, ubv = _bounds(lb, ub, self.dim)
-        opts, self._keep = _opts(stream, rank, world, device, nccl_id, workspace)
+        opts, self._keep = _opts(stream, rank, world, device, nccl_id, workspace, flags,
+                                 peer_timeout_ms)
         h = ctypes.c_void_p()
         _check(lib().evox_pso_init(self.pop, self.dim, lbv.ctypes.data, ubv.ctypes.data,
                                    float(w), float(phi_p), float(phi_g),
@@ -433,11 +447,13 @@ class CSO(_Handle):
 
     def __init__(self, pop: int, dim: int, lb=-5.12, ub=5.12, phi: float = 0.0, block: int = 0,
                  seed: int = 0, stream=None, rank: int = 0, world: int = 1,
-                 nccl_id: Optional[bytes] = None, device: Optional[int] = None, workspace=None):
+                 nccl_id: Optional[bytes] = None, device: Optional[int] = None, workspace=None,
+                 flags: int = 0, peer_timeout_ms: Optional[int] = None):
         self._h = None
         self.pop, self.dim = int(pop), int(dim)
         lbv, ubv = _bounds(lb, ub, self.dim)
-        opts, self._keep = _opts(stream, rank, world, device, nccl_id, workspace)
+        opts, self._keep = _opts(stream, rank, world, device, nccl_id, workspace, flags,
+                                 peer_timeout_ms)
         h = ctypes.c_void_p()
         _check(lib().evox_cso_init(self.pop, self.dim, lbv.ctypes.data, ubv.ctypes.data,
                                    float(phi), int(block), int(seed) & 0xFFFFFFFFFFFFFFFF,
@@ -479,11 +495,13 @@ class DE(_Handle):
 
     def __init__(self, pop: int, dim: int, lb=-5.12, ub=5.12, F: float = 0.5, CR: float = 0.9,
                  seed: int = 0, stream=None, rank: int = 0, world: int = 1,
-                 device: Optional[int] = None, workspace=None):
+                 device: Optional[int] = None, workspace=None, flags: int = 0,
+                 peer_timeout_ms: Optional[int] = None):
         self._h = None
         self.pop, self.dim = int(pop), int(dim)
         lbv, ubv = _bounds(lb, ub, self.dim)
-        opts, self._keep = _opts(stream, rank, world, device, None, workspace)
+        opts, self._keep = _opts(stream, rank, world, device, None, workspace, flags,
+                                 peer_timeout_ms)
         h = ctypes.c_void_p()
         _check(lib().evox_de_init(self.pop, self.dim, lbv.ctypes.data, ubv.ctypes.data, float(F),
                                   float(CR), int(seed) & 0xFFFFFFFFFFFFFFFF, ctypes.byref(opts),

@@ -4,11 +4,14 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-# peer-memory exchanges under test give up after 20 s instead of 60 s, so a broken
-# peer test fails fast instead of stalling the run (EVOX_ERR_EXCHANGE)
-os.environ.setdefault("EVOX_PEER_TIMEOUT_MS", "20000")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+
+# peer-memory exchanges under test give up after 20 s instead of 60 s, so a broken
+# peer test fails fast instead of stalling the run (EVOX_ERR_EXCHANGE)
+from paper_2301_12457_b200 import evox as _evox  # noqa: E402
+
+_evox.DEFAULT_PEER_TIMEOUT_MS = 20000
 
 
 def pytest_configure(config):

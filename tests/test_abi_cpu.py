@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_version_and_abi():
     assert "evox" in ev.version()
-    assert ev.lib().evox_abi_version() == 1
+    assert ev.lib().evox_abi_version() == 2
 
 
 @pytest.mark.parametrize("pop,world", [(100, 4), (10, 4), (7, 3), (1, 1), (5, 8), (1000003, 8)])

@@ -140,6 +140,11 @@ def test_de_config_errors():
         ev.DE(3, 4, -1, 1)
     with pytest.raises(E.InvalidArgument):
         ev.DE(10, 4, -1, 1, CR=1.5)
+    for F in (0.0, -0.5, 2.5, float("nan")):  # SPEC de_setup: F in (0, 2]
+        with pytest.raises(E.InvalidArgument):
+            ev.DE(10, 4, -1, 1, F=F)
+    assert ev.DE(10, 4, -1, 1, F=2.0).best(with_row=False)[:2] == (float("inf"), -1)
+    assert ev.CSO(16, 4, -1, 1).best(with_row=False)[:2] == (float("inf"), -1)
     de = ev.DE(10, 4, -1, 1)
     de.step("sphere", 1)
     with pytest.raises(E.ContractError):

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from parity import (assert_fitness, assert_positions, compare_pso, gpu_pso_state,
+from parity import (assert_fitness, assert_positions, compare_pso, gpu_pso_state, near_tie,
                     resync_oracle_from_gpu)
 
 torch = pytest.importorskip("torch")
@@ -18,6 +18,7 @@ pytestmark = pytest.mark.gpu
 import paper_2301_12457_b200 as ev  # noqa: E402
 from paper_2301_12457_b200 import evox as E  # noqa: E402
 from paper_2301_12457_b200 import workloads as WL  # noqa: E402
+from test_gpu_sharded_oracle import cso_flipped_pairs_are_near_ties  # noqa: E402
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -168,13 +169,12 @@ def test_pso_graphed_equals_stepwise(problem, N, D, lb, ub, seed):
 
 
 @pytest.mark.parametrize("problem,N,D,lb,ub,seed", PSO_CASES[:5])
-def test_pso_small_kernel_equals_grid_kernel(problem, N, D, lb, ub, seed, monkeypatch):
+def test_pso_small_kernel_equals_grid_kernel(problem, N, D, lb, ub, seed):
     """The persistent single-CTA kernel (tiny populations) is bitwise identical to the
     multi-CTA generation kernel."""
     a = ev.PSO(N, D, lb, ub, seed=seed)
     a.step(problem, 60)
-    monkeypatch.setenv("EVOX_NO_SMALL", "1")
-    b = ev.PSO(N, D, lb, ub, seed=seed)
+    b = ev.PSO(N, D, lb, ub, seed=seed, flags=E.FLAG_NO_SMALL)
     b.step(problem, 60)
     ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
     for k in ("X", "V", "P", "f", "pf", "G", "hist"):
@@ -187,17 +187,15 @@ def test_pso_small_kernel_equals_grid_kernel(problem, N, D, lb, ub, seed, monkey
                                          ("griewank", 1999, 250),     # 8 lanes per row
                                          ("rastrigin", 21, 5000),     # CTA per row
                                          ("sphere", 700, 1001)])      # ragged tail
-def test_pso_mid_kernel_equals_stepwise(problem, N, D, monkeypatch):
+def test_pso_mid_kernel_equals_stepwise(problem, N, D):
     """The persistent cooperative kernel (mid-size populations, n generations in one launch,
     grid barrier between generations) is bitwise identical to one k_pso_gen launch per
     generation; two step calls exercise the barrier epoch across launches."""
     lb, ub = WL.BOUNDS[problem]
-    monkeypatch.delenv("EVOX_NO_MID", raising=False)
     a = ev.PSO(N, D, lb, ub, seed=31)
     a.step(problem, 10)
     a.step(problem, 15)
-    monkeypatch.setenv("EVOX_NO_MID", "1")
-    b = ev.PSO(N, D, lb, ub, seed=31)
+    b = ev.PSO(N, D, lb, ub, seed=31, flags=E.FLAG_NO_MID)
     b.step(problem, 25)
     ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
     for k in ("X", "V", "P", "f", "pf", "G", "hist"):
@@ -208,16 +206,13 @@ def test_pso_mid_kernel_equals_stepwise(problem, N, D, monkeypatch):
 @pytest.mark.parametrize("problem,N,D", [("ackley", 300, 1000), ("rosenbrock", 77, 1001),
                                          ("griewank", 64, 4096), ("rastrigin", 130, 600),
                                          ("sphere", 1000, 300)])
-def test_pso_tma_kernel_equals_ldg_kernel(problem, N, D, monkeypatch):
+def test_pso_tma_kernel_equals_ldg_kernel(problem, N, D):
     """The TMA-staged generation kernel (opt-in, warp-per-row geometry) is bitwise identical
     to the default LDG kernel."""
     lb, ub = WL.BOUNDS[problem]
-    monkeypatch.setenv("EVOX_NO_SMALL", "1")
-    monkeypatch.setenv("EVOX_TMA", "1")
-    a = ev.PSO(N, D, lb, ub, seed=12)
+    a = ev.PSO(N, D, lb, ub, seed=12, flags=E.FLAG_NO_SMALL | E.FLAG_TMA)
     a.step(problem, 9)
-    monkeypatch.setenv("EVOX_TMA", "0")
-    b = ev.PSO(N, D, lb, ub, seed=12)
+    b = ev.PSO(N, D, lb, ub, seed=12, flags=E.FLAG_NO_SMALL)
     b.step(problem, 9)
     ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
     for k in ("X", "V", "P", "f", "pf", "G", "hist"):
@@ -334,14 +329,13 @@ def test_pso_user_stream_and_workspace():
     assert a.info()["stream"] == s.cuda_stream
 
 
-def test_pso_nccl_exchange_path_single_rank(monkeypatch):
-    """EVOX_FORCE_NCCL=1: the multi-GPU exchange (record all-gather + gbest select) on a
+def test_pso_nccl_exchange_path_single_rank():
+    """EVOX_FLAG_FORCE_NCCL: the multi-GPU exchange (record all-gather + gbest select) on a
     1-rank communicator gives the same trajectory bitwise as the direct path."""
     N, D, p = 96, 50, "ackley"
     a = ev.PSO(N, D, -32.768, 32.768, seed=21)
     a.step(p, 15)
-    monkeypatch.setenv("EVOX_FORCE_NCCL", "1")
-    b = ev.PSO(N, D, -32.768, 32.768, seed=21)
+    b = ev.PSO(N, D, -32.768, 32.768, seed=21, flags=E.FLAG_FORCE_NCCL)
     b.step(p, 15)
     ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
     for k in ("X", "V", "P", "f", "pf", "G", "hist"):
@@ -350,52 +344,70 @@ def test_pso_nccl_exchange_path_single_rank(monkeypatch):
 
 
 # ---------------------------------------------------- full-size sampled checks
-def _sampled_generation_check(problem, N, D, seed, n_sample=64):
-    """At full size: run generation 0 (+ one move) on the GPU, recompute sampled rows
-    one by one with the oracle from the GPU's pre-move state, and check argmin
-    properties on the whole population."""
+def _sampled_generations_check(problem, N, D, seed, gens=10, n_sample=256, threads=8):
+    """At full size, stepped from identical states (north_star: 1 and 10 generations):
+    generation 0, then every generation re-derive sampled rows one by one with the oracle
+    from the GPU's PRE-move state (X, V, materialised pbest P, gbest G, t) -- positions and
+    velocities bitwise, fitness within tolerance, the pbest decision of each sampled row --
+    and check the tell on the whole population (gbest strict improvement, lowest index,
+    hist)."""
     lb, ub = WL.BOUNDS[problem]
     pso = ev.PSO(N, D, lb, ub, seed=seed)
     pso.step(problem, 0)
     rng = np.random.default_rng(seed)
     rows = np.unique(np.concatenate([[0, N - 1], rng.integers(0, N, n_sample)]))
-    Xv = pso.view("X")
-    X0 = Xv[rows].cpu().numpy()[:, :D].copy()
-    V0 = pso.view("V")[rows].cpu().numpy()[:, :D].copy()
-    P0 = pso.view("P")[rows].cpu().numpy()[:, :D].copy()
-    G0 = pso.view("G").cpu().numpy()[:D].copy()
+    ridx = torch.from_numpy(rows).cuda()
+    take = lambda k: pso.view(k)[ridx].cpu().numpy()[:, :D].copy()  # noqa: E731
     f0 = pso.view("F").cpu().numpy()
-    # generation 0 properties: the argmin over the whole population
     gf, gi, grow = pso.best()
     m = f0.min()
     assert gf == m and gi == int(np.nonzero(f0 == m)[0][0])
     assert np.array_equal(grow, pso.view("X")[gi].cpu().numpy()[:D])
-    assert_fitness(f0[rows], O.evaluate(problem, X0), "gen0 sampled f")
-    pso.step(problem, 1)
-    X1 = pso.view("X")[rows].cpu().numpy()[:, :D]
-    V1 = pso.view("V")[rows].cpu().numpy()[:, :D]
-    f1 = pso.view("F").cpu().numpy()
-    for k, r in enumerate(rows):
-        x, v = X0[k:k + 1].copy(), V0[k:k + 1].copy()
-        O.pso_move(x, v, P0[k:k + 1], G0, int(r), 0, seed, WL.W, WL.PHI_P, WL.PHI_G, lb, ub)
-        assert np.array_equal(X1[k], x[0]), f"row {r} X"
-        assert np.array_equal(V1[k], v[0]), f"row {r} V"
-    assert_fitness(f1[rows], O.evaluate(problem, X1), "gen1 sampled f")
-    gf1, gi1, _ = pso.best(with_row=False)
-    assert gf1 == min(gf, f1.min())
-    h = pso.history()
-    assert len(h) == 2 and h[0] == f0.min() and h[1] == f1.min()
+    assert_fitness(f0[rows], O.evaluate(problem, take("X"), threads), "gen0 sampled f")
+    for t in range(gens):
+        X0, V0, P0 = take("X"), take("V"), take("P")
+        pf0 = pso.view("PF")[ridx].cpu().numpy().copy()
+        G0 = pso.view("G").cpu().numpy()[:D].copy()
+        gf0 = pso.best(with_row=False)[0]
+        pso.step(problem, 1)
+        X1, V1, P1 = take("X"), take("V"), take("P")
+        f1 = pso.view("F").cpu().numpy()
+        pf1 = pso.view("PF")[ridx].cpu().numpy()
+        x, v = X0.copy(), V0.copy()
+        for k, r in enumerate(rows):
+            O.pso_move(x[k:k + 1], v[k:k + 1], P0[k:k + 1], G0, int(r), t, seed, WL.W, WL.PHI_P,
+                       WL.PHI_G, lb, ub)
+        assert np.array_equal(X1, x), f"t={t + 1}: sampled X"
+        assert np.array_equal(V1, v), f"t={t + 1}: sampled V"
+        F64 = O.evaluate(problem, X1, threads)
+        assert_fitness(f1[rows], F64, f"t={t + 1}: sampled f")
+        for k, r in enumerate(rows):  # pbest (S:316 strict), unless a near-tie
+            imp = f1[r] < pf0[k]
+            if near_tie(f1[r], pf0[k]):
+                continue
+            assert np.array_equal(P1[k], X1[k] if imp else P0[k]), (t, r)
+            assert pf1[k] == (f1[r] if imp else pf0[k]), (t, r)
+        gf1, gi1, grow1 = pso.best()
+        m = f1.min()
+        if m < gf0:  # strict improvement, lowest index among equal minima
+            assert gf1 == m and gi1 == int(np.nonzero(f1 == m)[0][0])
+            assert np.array_equal(grow1, pso.view("X")[gi1].cpu().numpy()[:D])
+        else:
+            assert gf1 == gf0
+        h = pso.history()
+        assert len(h) == t + 2 and h[-1] == m
     pso.close()
 
 
 @pytest.mark.parametrize("cfg", ["C2", "C4g", "C4r", "C5", "H"])
-def test_full_size_sampled(cfg):
+def test_full_size_sampled_10_gens(cfg):
     c = WL.CONFIGS[cfg]
     free, _ = torch.cuda.mem_get_info()
     need = 3 * c.pop * WL.round4(c.dim) * 4 * 1.1
     if need > free:
         pytest.skip("not enough device memory")
-    _sampled_generation_check(c.problem, c.pop, c.dim, seed=0)
+    _sampled_generations_check(c.problem, c.pop, c.dim, seed=0, gens=10,
+                               n_sample=64 if c.dim > 10_000 else 256)
 
 
 def test_c2_full_parity_10_gens():
@@ -419,6 +431,7 @@ def _cso_parity(problem, N, D, B, seed, gens, phi=0.0):
     hist = [float(f.min())]
     resync = 0
     for t in range(gens):
+        f_prev = f.copy()
         cso.step(problem, 1)
         O.cso_generation(problem, X, V, f, F64, B, t, seed, lb, ub, phi=phi)
         hist.append(float(f.min()))
@@ -426,7 +439,8 @@ def _cso_parity(problem, N, D, B, seed, gens, phi=0.0):
         Vg = cso.view("V").cpu().numpy()[:, :D]
         fg = cso.view("F").cpu().numpy()
         if not np.array_equal(Xg, X):
-            # a flipped winner at a near-tie: adopt the GPU state (R-9) -- must be rare
+            # a flipped winner: only at a near-tie of the pair (R-9) -- then adopt the GPU state
+            cso_flipped_pairs_are_near_ties(Xg, X, f_prev, N, B, t, seed)
             resync += 1
             X, V, f = Xg.copy(), Vg.copy(), fg.copy()
             F64 = O.evaluate(problem, X)
@@ -460,57 +474,63 @@ def test_cso_phi_nonzero_parity_many_chunks(problem, N, D, B, phi):
     assert _cso_parity(problem, N, D, B, seed=11, gens=6, phi=phi) <= 1
 
 
-def test_cso_phi_nccl_path_single_rank(monkeypatch):
+def test_cso_phi_nccl_path_single_rank():
     N, D, p = 256, 40, "ackley"
     a = ev.CSO(N, D, -32.768, 32.768, phi=0.2, block=32, seed=8)
     a.step(p, 12)
-    monkeypatch.setenv("EVOX_FORCE_NCCL", "1")
-    b = ev.CSO(N, D, -32.768, 32.768, phi=0.2, block=32, seed=8)
+    b = ev.CSO(N, D, -32.768, 32.768, phi=0.2, block=32, seed=8, flags=E.FLAG_FORCE_NCCL)
     b.step(p, 12)
     assert np.array_equal(a.view("X").cpu().numpy(), b.view("X").cpu().numpy())
     assert np.array_equal(a.history(), b.history())
 
 
-def test_cso_nccl_path_single_rank(monkeypatch):
+def test_cso_nccl_path_single_rank():
     N, D, p = 128, 40, "rastrigin"
     a = ev.CSO(N, D, -5.12, 5.12, block=16, seed=8)
     a.step(p, 12)
-    monkeypatch.setenv("EVOX_FORCE_NCCL", "1")
-    b = ev.CSO(N, D, -5.12, 5.12, block=16, seed=8)
+    b = ev.CSO(N, D, -5.12, 5.12, block=16, seed=8, flags=E.FLAG_FORCE_NCCL)
     b.step(p, 12)
     assert np.array_equal(a.view("X").cpu().numpy(), b.view("X").cpu().numpy())
     assert np.array_equal(a.history(), b.history())
     assert a.best()[:2] == b.best()[:2]
 
 
-def test_cso_c3_sampled():
-    """C3 (CSO/Rastrigin 1e5 x 1000): one generation, sampled pairs recomputed by the oracle."""
+def test_cso_c3_sampled_10_gens():
+    """C3 (CSO/Rastrigin 1e5 x 1000, B = pop/8): 10 generations; every generation sampled
+    pairs are recomputed one by one by the oracle from the GPU's pre-generation state
+    (winner bitwise unchanged, loser update bitwise, loser fitness within tolerance)."""
     c = WL.CONFIGS["C3"]
     lb, ub = WL.BOUNDS[c.problem]
     B = c.pop // 8
     cso = ev.CSO(c.pop, c.dim, lb, ub, block=B, seed=0)
     cso.step(c.problem, 0)
-    X0 = cso.view("X").cpu().numpy()[:, :c.dim].copy()
-    f0 = cso.view("F").cpu().numpy().copy()
-    cso.step(c.problem, 1)
-    X1 = cso.view("X").cpu().numpy()[:, :c.dim]
-    V1 = cso.view("V").cpu().numpy()[:, :c.dim]
-    f1 = cso.view("F").cpu().numpy()
-    changed = (X1 != X0).any(1)
-    assert changed.sum() <= c.pop // 2
     rng = np.random.default_rng(0)
-    for blk in (0, 7):
-        pairs = O.cso_pairs(B, blk, 0, 0)
-        for a, b in pairs[rng.integers(0, len(pairs), 8)]:
-            i, k = blk * B + a, blk * B + b
-            w, l = (i, k) if (f0[i] < f0[k] or (f0[i] == f0[k] and i < k)) else (k, i)
-            assert np.array_equal(X1[w], X0[w])
-            xl, vl = X0[l].copy(), np.zeros(c.dim, np.float32)
-            R1 = O.draw(1, c.dim, l, 0, 5, 0)[0]
-            R2 = O.draw(1, c.dim, l, 0, 6, 0)[0]
-            O.cso_loser_update_with(X0[w], xl, vl, R1, R2, lb=lb, ub=ub)
-            assert np.array_equal(X1[l], xl) and np.array_equal(V1[l], vl)
-    assert_fitness(f1[changed][:256], O.evaluate(c.problem, X1[changed][:256]), "C3 f")
+    for t in range(10):
+        X0 = cso.view("X").cpu().numpy()[:, :c.dim].copy()
+        V0 = cso.view("V").cpu().numpy()[:, :c.dim].copy()
+        f0 = cso.view("F").cpu().numpy().copy()
+        cso.step(c.problem, 1)
+        X1 = cso.view("X").cpu().numpy()[:, :c.dim]
+        V1 = cso.view("V").cpu().numpy()[:, :c.dim]
+        f1 = cso.view("F").cpu().numpy()
+        changed = (X1 != X0).any(1)
+        assert changed.sum() <= c.pop // 2
+        for blk in rng.choice(8, 2, replace=False):
+            pairs = O.cso_pairs(B, int(blk), t, 0)
+            for a, b in pairs[rng.integers(0, len(pairs), 8)]:
+                i, k = blk * B + a, blk * B + b
+                if near_tie(f0[i], f0[k]):
+                    continue
+                w, l = (i, k) if (f0[i] < f0[k] or (f0[i] == f0[k] and i < k)) else (k, i)
+                assert np.array_equal(X1[w], X0[w]) and np.array_equal(V1[w], V0[w])
+                xl, vl = X0[l].copy(), V0[l].copy()
+                R1 = O.draw(1, c.dim, int(l), t, 5, 0)[0]
+                R2 = O.draw(1, c.dim, int(l), t, 6, 0)[0]
+                O.cso_loser_update_with(X0[w], xl, vl, R1, R2, lb=lb, ub=ub)
+                assert np.array_equal(X1[l], xl) and np.array_equal(V1[l], vl), (t, l)
+                assert_fitness(f1[[l]], O.evaluate(c.problem, xl[None]), f"C3 t={t + 1} f")
+        assert (f1[~changed] == f0[~changed]).all()
+        assert cso.history()[-1] == f1.min() <= f0.min()
 
 
 # ------------------------------------------------------------- edge cases
@@ -546,11 +566,9 @@ def _run_parity_bounds(problem, N, D, lb, ub, seed, gens):
 
 
 @pytest.mark.parametrize("N,D", [(1, 1), (1, 7), (2, 1), (3, 5), (1, 1000)])
-def test_pso_degenerate_sizes(N, D, monkeypatch):
-    for small in ("0", "1"):
-        if small == "1":
-            monkeypatch.setenv("EVOX_NO_SMALL", "1")
-        pso = ev.PSO(N, D, -2, 2, seed=4)
+def test_pso_degenerate_sizes(N, D):
+    for flags in (0, E.FLAG_NO_SMALL):
+        pso = ev.PSO(N, D, -2, 2, seed=4, flags=flags)
         pso.step("rastrigin", 9)
         st = O.pso_run("rastrigin", N, D, -2, 2, seed=4, n_gens=9)
         g = gpu_pso_state(pso, D)
@@ -684,14 +702,13 @@ def test_cso_straddling_blocks_require_connect():
 @pytest.mark.parametrize("problem,N,D", [("ackley", 200, 1000), ("rosenbrock", 300, 100),
                                          ("griewank", 50, 4099), ("rastrigin", 70, 37),
                                          ("sphere", 9, 40001)])
-def test_fused_fitness_equals_evaluate(problem, N, D, monkeypatch):
+def test_fused_fitness_equals_evaluate(problem, N, D):
     """the fitness the fused generation kernel computes from registers is
     bitwise the standalone Problem.evaluate of the same population (same per-row
     reduction order: a function of dim only) -- for CSO whenever its row geometry is
     evaluate's (else within the fitness tolerance)."""
     lb, ub = WL.BOUNDS[problem]
-    monkeypatch.setenv("EVOX_NO_SMALL", "1")
-    pso = ev.PSO(N, D, lb, ub, seed=1)
+    pso = ev.PSO(N, D, lb, ub, seed=1, flags=E.FLAG_NO_SMALL)
     pso.step(problem, 3)
     X = pso.view("X")
     f = ev.evaluate(problem, X.clone(), dim=D).cpu().numpy()
@@ -713,12 +730,11 @@ def test_fused_fitness_equals_evaluate(problem, N, D, monkeypatch):
 
 
 @pytest.mark.parametrize("N,D", [(8, 4099), (3, 40001), (5, 100000)])
-def test_griewank_table_equals_per_element(N, D, monkeypatch):
+def test_griewank_table_equals_per_element(N, D):
     """evox_eval's global Griewank column table (CTA-per-row geometry, ld > 4096) holds
     griewank_h(j) itself: bitwise the per-element computation it replaces."""
     X = torch.from_numpy(WL.padded(WL.uniform_rows(N, D, "griewank", seed=D))).cuda()
     a = ev.evaluate("griewank", X, dim=D).cpu().numpy()
-    monkeypatch.setenv("EVOX_NO_HTAB", "1")
-    b = ev.evaluate("griewank", X, dim=D).cpu().numpy()
+    b = ev.evaluate("griewank", X, dim=D, flags=E.EVAL_NO_HTAB).cpu().numpy()
     assert np.array_equal(a, b)
     assert_fitness(a, O.evaluate("griewank", X.cpu().numpy()[:, :D]), f"griewank {N}x{D}")

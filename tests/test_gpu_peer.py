@@ -22,8 +22,8 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
-def _group(W, N, D, lb, ub, seed):
-    hs = [ev.PSO(N, D, lb, ub, seed=seed, rank=r, world=W, stream=torch.cuda.Stream())
+def _group(W, N, D, lb, ub, seed, **kw):
+    hs = [ev.PSO(N, D, lb, ub, seed=seed, rank=r, world=W, stream=torch.cuda.Stream(), **kw)
           for r in range(W)]
     boxes = [h.mailbox()[0] for h in hs]
     for h in hs:
@@ -81,9 +81,8 @@ def test_peer_group_ask_tell():
     assert hs[0].best()[:2] == ref.best()[:2]
 
 
-def test_peer_timeout_reports_exchange_error(monkeypatch):
-    monkeypatch.setenv("EVOX_PEER_TIMEOUT_MS", "1500")
-    hs = _group(2, 16, 8, -1, 1, 1)
+def test_peer_timeout_reports_exchange_error():
+    hs = _group(2, 16, 8, -1, 1, 1, peer_timeout_ms=1500)
     hs[0].step("sphere", 0)          # rank 1 never steps
     with pytest.raises(E.ExchangeError):
         hs[0].sync()

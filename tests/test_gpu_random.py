@@ -11,7 +11,9 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2301_12457_b200 as ev  # noqa: E402
+from paper_2301_12457_b200 import evox as E  # noqa: E402
 from paper_2301_12457_b200 import workloads as WL  # noqa: E402
+from test_gpu_sharded_oracle import cso_flipped_pairs_are_near_ties  # noqa: E402
 
 PROBLEMS = list(WL.BOUNDS)
 _rng = np.random.default_rng(20260417)
@@ -31,16 +33,14 @@ def _cuda():
 
 
 @pytest.mark.parametrize("k,problem,N,D,seed", CASES)
-def test_random_pso(k, problem, N, D, seed, monkeypatch):
+def test_random_pso(k, problem, N, D, seed):
     lo, hi = WL.BOUNDS[problem]
     if k % 3 == 0:  # per-dimension bounds
         lb = np.linspace(lo, lo / 2, D).astype(np.float32)
         ub = np.linspace(hi / 2, hi, D).astype(np.float32)
     else:
         lb, ub = lo, hi
-    if k % 2:
-        monkeypatch.setenv("EVOX_NO_SMALL", "1")
-    pso = ev.PSO(N, D, lb, ub, seed=seed)
+    pso = ev.PSO(N, D, lb, ub, seed=seed, flags=E.FLAG_NO_SMALL if k % 2 else 0)
     pso.step(problem, 0)
     st = O.pso_run(problem, N, D, lb, ub, seed=seed, n_gens=0)
     g = gpu_pso_state(pso, D)
@@ -63,16 +63,27 @@ def test_random_cso(k, problem, N, D, seed):
     cso = ev.CSO(N, D, lb, ub, block=B, seed=seed)
     cso.step(problem, 0)
     X, V, f, F64 = O.cso_init(problem, N, D, lb, ub, seed)
+    assert np.array_equal(cso.view("X").cpu().numpy()[:, :D], X)
     f = cso.view("F").cpu().numpy().copy()
+    resync = 0
     for t in range(4):
+        f_prev = f.copy()
         cso.step(problem, 1)
         O.cso_generation(problem, X, V, f, F64, B, t, seed, lb, ub)
         Xg = cso.view("X").cpu().numpy()[:, :D]
+        Vg = cso.view("V").cpu().numpy()[:, :D]
         fg = cso.view("F").cpu().numpy()
-        if not np.array_equal(Xg, X):  # near-tie winner flip: adopt the GPU state (R-9)
-            X, V = Xg.copy(), cso.view("V").cpu().numpy()[:, :D].copy()
+        if not np.array_equal(Xg, X):
+            # a flipped winner decision: only at a near-tie of that pair (R-9), then resync
+            cso_flipped_pairs_are_near_ties(Xg, X, f_prev, N, B, t, seed)
+            resync += 1
+            X, V = Xg.copy(), Vg.copy()
+        else:
+            assert np.array_equal(Vg, V)
         assert_fitness(fg, O.evaluate(problem, Xg), f"CSO t={t + 1}")
         f = fg.copy()
+        F64 = O.evaluate(problem, X)
+    assert resync <= 1
 
 
 @pytest.mark.parametrize("k,problem,N,D,seed", CASES[1::2])
