@@ -105,7 +105,9 @@ enum {
     EVOX_FLAG_TMA = 1u << 2,        /* PSO, 32 < ld/4 <= 1024: bulk-copy-staged generation kernel */
     EVOX_FLAG_FORCE_NCCL = 1u << 3, /* world == 1: run the NCCL exchange path on a 1-rank
                                        communicator (exercises the multi-GPU code) */
-    EVOX_FLAG_NO_GRAPH = 1u << 4    /* launch generations directly, not through CUDA graphs */
+    EVOX_FLAG_NO_GRAPH = 1u << 4,   /* launch generations directly, not through CUDA graphs */
+    EVOX_FLAG_NO_WAVE = 1u << 5     /* PSO, > 2^25 elements: the persistent grid-stride generation
+                                       kernel instead of the one-CTA-per-row-block wave grid */
 };
 
 /* Description of the last failure on the calling thread ("" if none). */

@@ -66,6 +66,8 @@ struct MoverCso {
         v[u] = ld_stream<EF>(Vl + q);
         xw[u] = ld_stream<EF>(Xw + q);
     }
+    template <bool EF>
+    __device__ __forceinline__ void load_late(int, int) {}
     __device__ __forceinline__ static float upd(float xl, float vl, float xwv, float r1, float r2,
                                                 float c3, float xb, bool use3, float lo, float hi,
                                                 float& vout) {

@@ -57,6 +57,8 @@ struct MoverDe {
         xb[u] = __ldcg(Xb + q);
         xc[u] = __ldcg(Xc + q);
     }
+    template <bool EF>
+    __device__ __forceinline__ void load_late(int, int) {}
     __device__ __forceinline__ static float trial(float xi, float va, float vb, float vc, float U,
                                                   float CR, float F, bool forced, float lo,
                                                   float hi) {

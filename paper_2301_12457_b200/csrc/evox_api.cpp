@@ -486,6 +486,10 @@ struct evox_pso : Base {
 
 namespace {
 
+bool pso_use_wave(const evox_pso* s) {
+    return !(s->flags & EVOX_FLAG_NO_WAVE) && evox::pso_wave(s->ld, s->rows);
+}
+
 void pso_layout(evox_pso* s, Carver& c) {
     const size_t mat = sizeof(float) * (size_t)s->rows * (size_t)s->ld;
     c.add(&s->X, mat);
@@ -654,7 +658,7 @@ evox_status evox_pso_init(int64_t pop, int64_t dim, const float* lb, const float
         }
         if (e != cudaSuccess) st = poison(s, EVOX_ERR_CUDA, "pso init", e);
         for (int p = 0; p < 5 && st == EVOX_OK; ++p)
-            s->gen_grid[p] = evox::pso_gen_grid(p, s->ld, s->rows, s->device);
+            s->gen_grid[p] = evox::pso_gen_grid(p, s->ld, s->rows, s->device, pso_use_wave(s));
     }
     if (st != EVOX_OK) {
         std::string keep = t_err;
@@ -708,7 +712,8 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
     }
     st = run_graphed(s, (int)problem, n_gens, [&]() -> evox_status {
         CU(s, timed(s, [&] { return evox::launch_pso_gen((int)problem, a, grid, s->stream,
-                                                      (s->flags & EVOX_FLAG_TMA) != 0); }));
+                                                      (s->flags & EVOX_FLAG_TMA) != 0,
+                                                      pso_use_wave(s)); }));
         return pso_exchange(s);
     });
     if (st != EVOX_OK) return st;

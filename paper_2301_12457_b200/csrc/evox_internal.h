@@ -127,7 +127,10 @@ cudaError_t launch_pso_init(const PsoArgs& a, cudaStream_t st);
 cudaError_t launch_eval(int problem, const float* X, long long rows, long long D, long long ld,
                         float* fit, cudaStream_t st, bool no_htab = false);
 // tma: the bulk-copy-staged variant (warp-per-row geometry only; EVOX_FLAG_TMA)
-cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st, bool tma);
+cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st, bool tma,
+                           bool wave);
+// Big populations take the wave grid (k_pso_gen_wave + k_pso_fin) unless no_wave.
+bool pso_wave(long long ld, long long rows);
 // Mode-A next-row L2 prefetch of the PSO generation (PsoArgs.pf_next): a schedule choice
 // measured per geometry and size, never a change of any result bit.
 bool pso_prefetch_next(long long ld, long long rows);
@@ -136,7 +139,7 @@ cudaError_t launch_pso_tell(const PsoArgs& a, const float* fit, unsigned long lo
                             cudaStream_t st);
 cudaError_t launch_gbest_select(const PsoArgs& a, cudaStream_t st);
 cudaError_t launch_pso_materialize(const PsoArgs& a, cudaStream_t st);
-int pso_gen_grid(int problem, long long ld, long long rows, int device);
+int pso_gen_grid(int problem, long long ld, long long rows, int device, bool wave);
 // Tiny populations: all generations in one single-CTA launch (bitwise identical).
 bool pso_small(long long rows, long long ld);
 cudaError_t launch_pso_run_small(int problem, const PsoArgs& a, long long n, cudaStream_t st);

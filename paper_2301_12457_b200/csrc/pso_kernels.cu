@@ -40,6 +40,9 @@ struct MoverPso {
     __device__ __forceinline__ void load(int u, int q) {
         x[u] = ld_stream<EF>(Xr + q);
         v[u] = ld_stream<EF>(Vr + q);
+    }
+    template <bool EF>
+    __device__ __forceinline__ void load_late(int u, int q) {  // waits for imp (pend)
         if (!pend) p[u] = ld_stream<EF>(Pr + q);
     }
     __device__ __forceinline__ float4 step(int u, int q) {
@@ -328,6 +331,78 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : (G::LPR == 4
     const unsigned long long best = pso_gen_rows<P, G, UNI, false>(a, m, t, htab, sh_acc, sh_head);
     unsigned long long key;
     if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
+}
+
+#ifndef EVOX_WAVE_MINB
+#define EVOX_WAVE_MINB 3
+#endif
+#ifndef EVOX_WAVE_U
+#define EVOX_WAVE_U 3  // chunks in flight per lane group in the wave kernel
+#endif
+
+// Fused PSO generation on a "wave" grid: one CTA per row block (every thread at most one
+// row), CTAs scheduled by the hardware in row order as slots free up.  Per row it runs
+// exactly the code of k_pso_gen (same geometry, reduction order and decisions: bitwise the
+// same trajectory); what it drops is the persistent loop's state (prefetch windows,
+// next-row flags) and the end-of-grid fence + ticket: a CTA's minimum key goes to
+// ctl->gen_key with one relaxed atomicMin, and the gbest publication runs in k_pso_fin,
+// ordered after this grid by the kernel boundary (PDL griddepcontrol.wait).  The P load
+// of a row waits on its imp flag; X and V of the row are already in flight by then
+// (walk_segment's late loads).  Micro (profiles/r02_micro_np3.txt): this schedule streams
+// the generation's access pattern at 6.48 TB/s against 6.13-6.33 for a persistent grid.
+template <int P, class G, bool UNI>
+__global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : EVOX_WAVE_MINB)
+    k_pso_gen_wave(PsoArgs a) {
+    __shared__ Fit<P> sh_acc[G::WPR];
+    __shared__ float sh_head[G::WPR];
+    __shared__ __align__(16) HStore<P, G> sh_h;
+    __shared__ unsigned long long sh_k[WARPS];
+    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+    const RowMap<G> m(a.ld >> 2);
+    const long long row = m.first;  // grid = row units: at most one row per thread
+    const bool ok = row < a.rows;
+    pdl_wait();               // the previous generation (G, imp, pf, t) is complete
+    pdl_launch_dependents();
+    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
+    const bool pend = ok ? a.imp[row] != 0 : true;
+    float pf_old = 0.0f;
+    if (m.leader && ok) pf_old = a.pf[row];
+    unsigned long long best = ~0ull;
+    if (m.wfirst < a.rows) {  // warp-uniform (CTA-uniform for WPR > 1)
+        MoverPso<UNI, false> mv(a, ok ? row : 0, (uint32_t)t, pend);
+        Fit<P> acc;
+        float hx, tx;
+        bool tv;
+        NoPrefetch pf;
+        walk_segment<P, G>(mv, m.qb, m.qe, a.D, ok, acc, hx, tx, tv, pf, htab);
+        const float f = reduce_row<P, G>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
+        if (m.leader && ok) {
+            const bool imp = f < pf_old;  // per-row tell (A11): strict, NaN never improves
+            a.f[row] = f;
+            a.imp[row] = imp ? 1 : 0;
+            if (imp) a.pf[row] = f;
+            best = make_key(f, a.row0 + row);
+        }
+    }
+    best = warp_min_u64(best);
+    if (lane_id() == 0) sh_k[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long k = sh_k[0];
+#pragma unroll
+        for (int i = 1; i < WARPS; ++i) k = sh_k[i] < k ? sh_k[i] : k;
+        if (k != ~0ull) atomicMin(&a.ctl->gen_key, k);
+    }
+}
+
+// gbest publication of a wave generation (one CTA): the last-CTA step of k_pso_gen --
+// strict improvement, hist, t; or the winner record / peer exchange for world > 1.
+__global__ void __launch_bounds__(256) k_pso_fin(PsoArgs a) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
+    const unsigned long long key = *(volatile unsigned long long*)&a.ctl->gen_key;
+    pso_finalize(a, key, t + 1);
 }
 
 #ifndef EVOX_MID_PF
@@ -793,13 +868,32 @@ constexpr long long BIG = 1LL << 25;
 // bytes and cost 4 points at H: 0.863 -> 0.900 without it) and 4 waves of resident CTAs
 // (+0.6 points); short rows (4 / 8 lanes per row) and L2-sized populations keep the
 // prefetch (C4g 0.764 vs 0.706 without; C2 0.678 vs 0.637), profiles/r02_pf.txt.
+#ifndef EVOX_PF_NEXT
+#define EVOX_PF_NEXT -1  // measurement builds: 0 / 1 force the mode-A prefetch off / on
+#endif
 bool pso_prefetch_next(long long ld, long long rows) {
+    if (EVOX_PF_NEXT >= 0) return EVOX_PF_NEXT != 0;
     return !(geom_id(ld) == 1 && rows * ld > BIG);
 }
 
-int pso_gen_grid(int problem, long long ld, long long rows, int device) {
-    const int waves = geom_id(ld) == 1 && rows * ld > BIG ? 4 : 1;
+#ifndef EVOX_WAVE
+// which big populations take the wave grid (bit k: geometry id k; measurement builds may
+// change it).  Measured (profiles/r02_ab_wave.txt): CTA-per-row (C5) 0.895 -> 0.923 of the
+// HBM peak; warp-per-row (H) 0.898 -> 0.891 and 4-lanes-per-row (C4) 0.770 -> 0.664: those
+// keep the persistent grid.
+#define EVOX_WAVE (1 << 2)
+#endif
+bool pso_wave(long long ld, long long rows) {
+    return rows * ld > BIG && ((EVOX_WAVE >> geom_id(ld)) & 1);
+}
+
+int pso_gen_grid(int problem, long long ld, long long rows, int device, bool wave) {
     int g = 1;
+    if (wave) {
+        EVOX_DISPATCH_GEOM(ld, { g = (int)row_units<G_>(rows); });
+        return g;
+    }
+    const int waves = geom_id(ld) == 1 && rows * ld > BIG ? 4 : 1;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
         g = grid_for((const void*)k_pso_gen<P_, G_, true>, row_units<G_>(rows), device, waves);
     }));
@@ -815,8 +909,19 @@ static void tma_attr(K kernel) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
 }
 
-cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st, bool tma) {
+cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st, bool tma,
+                           bool wave) {
     cudaError_t e = cudaSuccess;
+    if (wave && !use_tma(a.ld, tma)) {
+        // the wave kernel keeps fewer chunks in flight (registers for 3 CTAs/SM); the chunk
+        // count never changes a lane's quad order, so the reduction order is the geometry's
+        EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+            using GW_ = Geom<G_::LPR, G_::WPR, G_::WPR == 1 ? EVOX_WAVE_U : G_::NU, G_::EFL>;
+            e = launch_pdl(k_pso_gen_wave<P_, GW_, U_>, grid, a, st);
+        })));
+        if (e == cudaSuccess) e = launch_pdl(k_pso_fin, 1, a, st);
+        return e != cudaSuccess ? e : cudaGetLastError();
+    }
     if (use_tma(a.ld, tma)) {
         EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, {
             tma_attr(k_pso_gen_tma<P_, U_>);

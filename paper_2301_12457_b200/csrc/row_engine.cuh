@@ -285,10 +285,19 @@ __device__ __forceinline__ void walk_segment(Mover& mv, long long qb_, long long
         const int q = base + G::LPR * u + sl;
         if (row_ok && q < qe) mv.template load<G::EFL>(u, q);
     };
+    // loads that depend on a late-arriving per-row flag (PSO: P unless the pbest copy is
+    // pending) go out after every independent load of the group, so the flag's latency
+    // overlaps the other loads instead of stalling them
+    auto load_late = [&](int u, int base) {
+        const int q = base + G::LPR * u + sl;
+        if (row_ok && q < qe) mv.template load_late<G::EFL>(u, q);
+    };
     for (int base = qb; base < qe; base += G::GROUP) {
         pf(base);
 #pragma unroll
         for (int u = 0; u < G::NU; ++u) load(u, base);
+#pragma unroll
+        for (int u = 0; u < G::NU; ++u) load_late(u, base);
         if constexpr (P == ROSENBROCK) {
             if (base + G::GROUP < qe && 4LL * (base + G::GROUP) < D) {  // warp-uniform
 #pragma unroll
@@ -376,6 +385,8 @@ struct MoverEval {
     float4 x[U];
     template <bool EF>
     __device__ __forceinline__ void load(int u, int q) { x[u] = ld_stream<EF>(Xr + q); }
+    template <bool EF>
+    __device__ __forceinline__ void load_late(int, int) {}
     __device__ __forceinline__ float4 step(int u, long long) { return x[u]; }
 };
 

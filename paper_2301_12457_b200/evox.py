@@ -62,7 +62,7 @@ class EvoxOpts(ctypes.Structure):
 
 
 # evox_opts.flags (include/evox.h): execution-path selectors that never change a result bit
-FLAG_NO_SMALL, FLAG_NO_MID, FLAG_TMA, FLAG_FORCE_NCCL, FLAG_NO_GRAPH = 1, 2, 4, 8, 16
+FLAG_NO_SMALL, FLAG_NO_MID, FLAG_TMA, FLAG_FORCE_NCCL, FLAG_NO_GRAPH, FLAG_NO_WAVE = 1, 2, 4, 8, 16, 32
 EVAL_NO_HTAB = 1
 # peer-memory exchange wait limit for new handles (0: the library default, 60 s)
 DEFAULT_PEER_TIMEOUT_MS = 0

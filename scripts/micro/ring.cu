@@ -173,6 +173,151 @@ __global__ void __launch_bounds__(256) k_np(St s) {
     }
 }
 
+// persistent grid-stride over rows (warp per row), the LDG pattern of the real kernel
+template <int PH>
+__global__ void __launch_bounds__(256) k_pers(St s) {
+    const int lane = threadIdx.x & 31;
+    for (long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); row < s.rows;
+         row += (long long)gridDim.x * 8) {
+        float4* X = s.X + row * s.nq;
+        float4* V = s.V + row * s.nq;
+        const float4* P = s.P + row * s.nq;
+        for (int b = 0; b < s.nq; b += 128) {
+            float4 x[4], v[4], p[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = b + 32 * u + lane;
+                if (q < s.nq) { x[u] = __ldcs(X + q); v[u] = __ldcs(V + q); p[u] = __ldcs(P + q); }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = b + 32 * u + lane;
+                if (q < s.nq) {
+                    compute<PH>(x[u], v[u], p[u], q, (uint32_t)row);
+                    __stcs(X + q, x[u]);
+                    __stcs(V + q, v[u]);
+                }
+            }
+        }
+    }
+}
+
+
+// np1 with the real kernel's extra work switched on feature by feature (bits of F):
+// 1 gbest row read per quad (__ldg, L1-resident 4 KB); 2 Ackley terms + row reduction +
+// f store; 4 per-row imp/pf read + write; 8 lazy pbest: rows flagged pending do not read
+// P but write P := X (45 % of rows, as at H).
+struct St2 { float4 *X, *V, *P; long long rows, nq; const float4* G; float* f; float* pf;
+             unsigned char* imp; };
+__device__ __forceinline__ float sinpi_red(float x) {
+    const float r = x - rintf(x);
+    const float z = r * r;
+    float p = fmaf(z, 0.0821458f, -0.5992645f);
+    p = fmaf(z, p, 2.5501640f);
+    p = fmaf(z, p, -5.1677128f);
+    p = fmaf(z, p, 3.1415927f);
+    return r * p;
+}
+template <int F, int MINB, int ORD = 0>
+__global__ void __launch_bounds__(256, MINB) k_np2(St2 s) {
+    const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= s.rows) return;
+    float4* X = s.X + row * s.nq;
+    float4* V = s.V + row * s.nq;
+    float4* P = s.P + row * s.nq;
+    bool pend = false;
+    float pf_old = 0.f;
+    if (F & 8) pend = s.imp[row] != 0;
+    if ((F & 4) && lane == 0) pf_old = s.pf[row];
+    float s2 = 0.f, ss = 0.f;
+    for (int b = 0; b < s.nq; b += 128) {
+        float4 x[4], v[4], p[4];
+        if (ORD) {  // X, V of the whole group first: pend is needed only for P
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = b + 32 * u + lane;
+                if (q < s.nq) { x[u] = __ldcs(X + q); v[u] = __ldcs(V + q); }
+            }
+            if (!pend) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int q = b + 32 * u + lane;
+                    if (q < s.nq) p[u] = __ldcs(P + q);
+                }
+            }
+        } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int q = b + 32 * u + lane;
+            if (q < s.nq) {
+                x[u] = __ldcs(X + q); v[u] = __ldcs(V + q);
+                if (!pend) p[u] = __ldcs(P + q);
+            }
+        }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int q = b + 32 * u + lane;
+            if (q < s.nq) {
+                float4 pb = pend ? x[u] : p[u];
+                if (pend) __stcs(P + q, x[u]);
+                if (F & 1) {
+                    const float4 g = __ldg(s.G + q);
+                    pb.x += g.x; pb.y += g.y; pb.z += g.z; pb.w += g.w;
+                }
+                compute<1>(x[u], v[u], pb, q, (uint32_t)row);
+                __stcs(X + q, x[u]);
+                __stcs(V + q, v[u]);
+                if (F & 2) {
+                    const float a[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) {
+                        s2 = fmaf(a[l], a[l], s2);
+                        const float sn = sinpi_red(a[l]);
+                        ss = fmaf(sn, sn, ss);
+                    }
+                }
+            }
+        }
+    }
+    if (F & 2) {
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) {
+            s2 += __shfl_xor_sync(0xffffffffu, s2, m);
+            ss += __shfl_xor_sync(0xffffffffu, ss, m);
+        }
+        if (lane == 0) s.f[row] = -20.f * expm1f(-0.2f * sqrtf(s2 / 1000.f)) - 2.718f * expm1f(-2.f * ss / 1000.f);
+    }
+    if ((F & 4) && lane == 0) {
+        const float fv = (F & 2) ? s.f[row] : s2;
+        const bool imp = fv < pf_old;
+        s.imp[row] = imp;
+        if (imp) s.pf[row] = fv;
+    }
+}
+
+template <class K, class S>
+void timeit2(const char* name, K kern, int grid, S s, double bytes) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float tot = 0;
+    const int n = 10;
+    for (int i = 0; i < 3 + n; ++i) {
+        if (i == 3) cudaEventRecord(a);
+        kern<<<grid, 256>>>(s);
+    }
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&tot, a, b);
+    printf("{\"case\": \"%s\", \"occ\": %d, \"ms\": %.4f, \"GBps\": %.1f, \"err\": \"%s\"}\n", name, occ,
+           tot / n, bytes / (tot / n * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    fflush(stdout);
+}
+
 template <class K>
 void timeit(const char* name, K kern, int grid, int block, int smem, St s, double bytes) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -211,31 +356,39 @@ int main() {
     cudaMalloc(&s.X, ab);
     cudaMalloc(&s.V, ab);
     cudaMalloc(&s.P, ab);
-    cudaMemset(s.X, 0, ab);
-    cudaMemset(s.V, 0, ab);
-    cudaMemset(s.P, 0, ab);
     const double b5 = 5.0 * ab;
     const int npg = (int)((s.rows + 7) / 8);
-    timeit("np1_ph0", k_np<0>, npg, 256, 0, s, b5);
+    St2 s2;
+    s2.X = s.X; s2.V = s.V; s2.P = s.P; s2.rows = s.rows; s2.nq = s.nq;
+    cudaMalloc(&s2.G, 16 * s.nq);
+    cudaMalloc(&s2.f, 4 * s.rows);
+    cudaMalloc(&s2.pf, 4 * s.rows);
+    cudaMalloc(&s2.imp, s.rows);
+    cudaMemset((void*)s2.G, 0, 16 * s.nq);
+    cudaMemset(s2.pf, 0, 4 * s.rows);
+    {   // 45 % of rows pending, pseudo-random
+        unsigned char* h = (unsigned char*)malloc(s.rows);
+        unsigned x = 12345;
+        for (long long i = 0; i < s.rows; ++i) { x = x * 1664525u + 1013904223u; h[i] = (x >> 24) < 115; }
+        cudaMemcpy(s2.imp, h, s.rows, cudaMemcpyHostToDevice);
+        free(h);
+    }
+    cudaMemset(s.X, 0x3f, ab);
+    cudaMemset(s.V, 0, ab);
+    cudaMemset(s.P, 0x3f, ab);
+    const double b4 = 4.0 * ab;
     timeit("np1_ph1", k_np<1>, npg, 256, 0, s, b5);
-    RING(8, 16, 0, 0, 1);
-    RING(8, 16, 1, 0, 1);
-    RING(8, 16, 0, 1, 1);
-    RING(8, 16, 1, 1, 1);
-    RING(12, 16, 0, 1, 1);
-    RING(12, 16, 1, 1, 1);
-    RING(16, 16, 0, 1, 1);
-    RING(16, 16, 1, 1, 1);
-    RING(4, 8, 0, 1, 2);
-    RING(4, 8, 1, 1, 2);
-    RING(6, 8, 0, 1, 2);
-    RING(6, 8, 1, 1, 2);
-    RING(8, 8, 1, 1, 2);
-    RING(4, 5, 1, 1, 3);
-    RING(3, 4, 1, 1, 4);
-    RING(16, 12, 1, 1, 1);
-    RING(8, 12, 1, 1, 1);
-    cudaError_t e = cudaDeviceSynchronize();
-    printf("{\"err\": \"%s\"}\n", cudaGetErrorString(e));
+    timeit2("np2_F8_m1", k_np2<8, 1>, npg, s2, b5);
+    timeit2("np2_F8_m1_ord", k_np2<8, 1, 1>, npg, s2, b5);
+    timeit2("np2_F8_m3_ord", k_np2<8, 3, 1>, npg, s2, b5);
+    timeit2("np2_F15_m2_ord", k_np2<15, 2, 1>, npg, s2, b5);
+    timeit2("np2_F15_m3_ord", k_np2<15, 3, 1>, npg, s2, b5);
+    {   // no row pending: F15 == the whole kernel at 3R2W
+        cudaMemset(s2.imp, 0, s.rows);
+        timeit2("np2_F15_m3_ord_nopend", k_np2<15, 3, 1>, npg, s2, b5);
+        cudaMemset(s2.imp, 1, s.rows);
+        timeit2("np2_F15_m3_ord_allpend", k_np2<15, 3, 1>, npg, s2, b5);
+    }
+    (void)b4;
     return 0;
 }

@@ -203,6 +203,47 @@ def test_pso_mid_kernel_equals_stepwise(problem, N, D):
     assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
 
 
+@pytest.mark.parametrize("problem,N,D", [("ackley", 400, 100_000), ("rosenbrock", 2000, 17_001),
+                                         ("griewank", 800, 50_000)])
+def test_pso_wave_kernel_equals_persistent(problem, N, D):
+    """Big populations (> 2^25 elements) run the wave grid (k_pso_gen_wave: one CTA per row
+    block, 3 chunks in flight, gbest published by k_pso_fin) -- bitwise the persistent
+    grid-stride kernel (EVOX_FLAG_NO_WAVE): same per-row code and reduction order."""
+    lb, ub = WL.BOUNDS[problem]
+    a = ev.PSO(N, D, lb, ub, seed=17)
+    a.step(problem, 4)
+    b = ev.PSO(N, D, lb, ub, seed=17, flags=E.FLAG_NO_WAVE)
+    b.step(problem, 4)
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
+        assert np.array_equal(ga[k], gb[k]), k
+    assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
+    a.close()
+    b.close()
+
+
+def test_pso_wave_kernel_peer_group():
+    """The wave grid with the in-kernel peer exchange (k_pso_fin runs it), W = 2 ranks of
+    4e7 elements each (CTA-per-row geometry), bitwise the single-shard persistent run."""
+    N, D, p = 800, 100_000, "ackley"
+    ref = ev.PSO(N, D, -32.768, 32.768, seed=2, flags=E.FLAG_NO_WAVE)
+    ref.step(p, 3)
+    hs = [ev.PSO(N, D, -32.768, 32.768, seed=2, rank=r, world=2, stream=torch.cuda.Stream())
+          for r in range(2)]
+    boxes = [h.mailbox()[0] for h in hs]
+    for h in hs:
+        h.connect_local(boxes)
+    for h in hs:
+        h.step(p, 3)
+    for h in hs:
+        h.sync()
+    X = np.concatenate([h.view("X").cpu().numpy() for h in hs])
+    assert np.array_equal(X, ref.view("X").cpu().numpy())
+    for h in hs:
+        assert h.best()[:2] == ref.best()[:2]
+        assert np.array_equal(h.history(), ref.history())
+
+
 @pytest.mark.parametrize("problem,N,D", [("ackley", 300, 1000), ("rosenbrock", 77, 1001),
                                          ("griewank", 64, 4096), ("rastrigin", 130, 600),
                                          ("sphere", 1000, 300)])
