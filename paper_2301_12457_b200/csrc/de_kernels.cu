@@ -107,6 +107,10 @@ __device__ __forceinline__ void de_finalize(const DeArgs& a, unsigned long long 
     }
 }
 
+#ifndef EVOX_DE_FIN
+#define EVOX_DE_FIN 0
+#endif
+
 // One DE generation: trial of every target from the population at parity p,
 // evaluation, greedy "<=" replacement by flipping the buffer-select flag.
 template <int P, class G, bool UNI>
@@ -193,8 +197,32 @@ __global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_DE_SHORT_MINB : EVOX_M
             best = k < best ? k : best;
         }
     }
+#if EVOX_DE_FIN
+    // the CTA's minimum key: one relaxed atomicMin, no fence / ticket (k_de_fin publishes
+    // after the kernel boundary)
+    __shared__ unsigned long long sh_k[WARPS];
+    best = warp_min_u64(best);
+    if (lane_id() == 0) sh_k[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long k = sh_k[0];
+#pragma unroll
+        for (int i = 1; i < WARPS; ++i) k = sh_k[i] < k ? sh_k[i] : k;
+        if (k != ~0ull) atomicMin(&a.ctl->gen_key, k);
+    }
+#else
     unsigned long long key;
     if (grid_argmin(a.ctl, best, &key, a.peer != 0)) de_finalize(a, key, t + 1);
+#endif
+}
+
+// End of a DE generation launched without the in-kernel grid argmin (EVOX_DE_FIN): the
+// generation's minimum, hist, and (peers) the end-of-generation barrier + global minimum.
+// The kernel boundary orders every row the generation wrote before the peer publication.
+__global__ void __launch_bounds__(32) k_de_fin(DeArgs a) {
+    if (a.peer) __threadfence_system();
+    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
+    de_finalize(a, *(volatile unsigned long long*)&a.ctl->gen_key, t + 1);
 }
 
 __global__ void k_de_init(DeArgs a) {
@@ -280,18 +308,32 @@ cudaError_t launch_de_tell0(const DeArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+#ifndef EVOX_DE_U
+#define EVOX_DE_U 2  // chunks in flight per lane group in the DE generation (short rows)
+#endif
+#ifndef EVOX_DE_WAVES
+#define EVOX_DE_WAVES 16
+#endif
+// The DE generation's geometry: the row geometry of ld with its own chunk count for short
+// rows (never a change of any lane's quad order, so the reduction order is the geometry's).
+#define EVOX_DE_GEOM(G_) Geom<G_::LPR, G_::WPR, G_::LPR == 4 ? EVOX_DE_U : G_::NU, G_::EFL>
+
 int de_gen_grid(int problem, long long ld, long long rows, int device) {
     int g = 1;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
-        g = grid_for((const void*)k_de_gen<P_, G_, true>, row_units<G_>(rows), device, 16);
+        using GD_ = EVOX_DE_GEOM(G_);
+        g = grid_for((const void*)k_de_gen<P_, GD_, true>, row_units<GD_>(rows), device,
+                     EVOX_DE_WAVES);
     }));
     return g;
 }
 
 cudaError_t launch_de_gen(int problem, const DeArgs& a, int grid, cudaStream_t st) {
     EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-        k_de_gen<P_, G_, U_><<<grid, 256, 0, st>>>(a);
+        using GD_ = EVOX_DE_GEOM(G_);
+        k_de_gen<P_, GD_, U_><<<grid, 256, 0, st>>>(a);
     })));
+    if (EVOX_DE_FIN) k_de_fin<<<1, 32, 0, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -50,7 +50,7 @@ namespace {
 #define EVOX_PSO_SHORT_MINB EVOX_MINB
 #endif
 #ifndef EVOX_DE_SHORT_MINB
-#define EVOX_DE_SHORT_MINB EVOX_MINB
+#define EVOX_DE_SHORT_MINB 3  // with 2 chunks in flight: D1 0.665 -> 0.713 (r02_ab_de.txt)
 #endif
 #ifndef EVOX_ROW_MINB
 #define EVOX_ROW_MINB 3  // CTA-per-row geometry (ld > 4096): C5 0.872 -> 0.909 (r02_pf.txt)
