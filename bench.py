@@ -44,13 +44,49 @@ def _env_int(k, d):
 def gen_kernel_name(cfg, rows, world):
     """The generation kernel evox_*_step launches for this shard (mirrors the C-ABI's
     dispatch: single-CTA persistent <= 2^16 elements, cooperative persistent <= 2^25 for
-    PSO at W = 1, else one k_*_gen launch per generation)."""
-    n = rows * ((cfg.dim + 3) // 4 * 4)
+    PSO at W = 1, the wave grid for PSO rows of > 4096 floats beyond 2^25 elements, else one
+    k_*_gen launch per generation)."""
+    ld = (cfg.dim + 3) // 4 * 4
+    n = rows * ld
     if cfg.algo == "pso" and world == 1 and n <= 65536:
         return f"k_pso_run_small<{cfg.problem}>"
     if cfg.algo == "pso" and world == 1 and n <= (1 << 25):
         return f"k_pso_run_mid<{cfg.problem}>"
+    if cfg.algo == "pso" and n > (1 << 25) and ld > 4096:
+        return f"k_pso_gen_wave<{cfg.problem}>"
     return f"k_{cfg.algo}_gen<{cfg.problem}>"
+
+
+NOMINAL_HBM_GBS = 8000.0  # B200 nominal (DGX figure; 7.7 TB/s HGX), context for "frac"
+
+
+def config_dict(cfg, world, exchange):
+    """The `config` of the JSON line -- identical in the GPU arm and the reference arm."""
+    par = f"row-sharded x{world}"
+    if world > 1:
+        kind = {"pso": "peer-memory key-first (in-kernel)" if exchange == "peer" else "nccl",
+                "cso": "peer-memory pairs" if exchange == "peer" else "nccl",
+                "de": "peer-memory donors", "eval": "none (independent rows)"}[cfg.algo]
+        par += f", exchange={kind}"
+    if cfg.algo == "eval":
+        l2 = "X (4 GB) > L2: inputs larger than L2, no flush needed"
+    else:
+        l2 = ("state (X,V,P) > L2: inputs larger than L2, no flush needed"
+              if 12 * cfg.pop * cfg.dim > 2 * 126e6 else "state comparable to L2")
+    return {"workload": cfg.note, "algo": cfg.algo, "problem": cfg.problem, "pop": cfg.pop,
+            "dim": cfg.dim, "seed": 1000 if cfg.algo == "eval" else 0, "parallelism": par,
+            "l2": l2}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def hbm_peak():
@@ -150,7 +186,8 @@ def ncu_traffic(cfg_name):
 
 def cpu_baseline(cfg, target_s=12.0):
     """The oracle as it stands, on the host cores, over a bounded row sample of the workload
-    (2 generations: move + evaluate + tell), extrapolated to whole-population gens/s."""
+    (2 generations: move + evaluate + tell), extrapolated to whole-population gens/s; the same
+    measured single-threaded on a smaller sample (nproc, CPU model, threads)."""
     cores = os.cpu_count() or 1
     D = cfg.dim
     rows = _sample_rows(cfg, cores, target_s / 2)
@@ -161,11 +198,19 @@ def cpu_baseline(cfg, target_s=12.0):
     t_gen = (time.perf_counter() - t0) / 2
     frac = rows / cfg.pop
     gens_per_s = frac / t_gen
+    rows1 = max(4, min(rows, _sample_rows(cfg, 1, 1.5)))
+    gen1 = _oracle_gen(cfg, rows1, 1)
+    t0 = time.perf_counter()
+    gen1(0)
+    t1 = time.perf_counter() - t0
     what = "2 evaluations" if cfg.algo == "eval" else "2 generations (move+eval+tell)"
     return {"value": gens_per_s, "unit": _unit(cfg), "cores": cores, "kind": "oracle",
             "sample": f"{rows} of {cfg.pop} rows x dim {D}, {what}, "
-                      f"{t_gen * 2:.2f} s; extrapolated linearly in rows",
-            "individual_dims_per_s": gens_per_s * cfg.pop * D * (0.5 if cfg.algo == "cso" else 1)}
+                      f"{t_gen * 2:.2f} s on {cores} threads; extrapolated linearly in rows",
+            "individual_dims_per_s": gens_per_s * cfg.pop * D * (0.5 if cfg.algo == "cso" else 1),
+            "cpu_model": cpu_model(), "nproc": cores,
+            "single_thread": {"value": (rows1 / cfg.pop) / t1, "unit": _unit(cfg),
+                              "sample": f"{rows1} rows, 1 generation, {t1:.2f} s"}}
 
 
 def _device_info(dev):
@@ -256,14 +301,12 @@ def run_eval(args, cfg, world, rank, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": cfg.note, "algo": "eval", "problem": cfg.problem,
-                       "pop": cfg.pop, "dim": cfg.dim, "seed": 1000,
-                       "parallelism": f"row-sharded x{world}",
-                       "l2": "X (4 GB) > L2: inputs larger than L2, no flush needed"},
+            "config": config_dict(cfg, world, args.exchange),
             "individual_dims_per_s": value * cfg.pop * cfg.dim,
             "bytes_per_generation": algorithmic_bytes(cfg, cfg.pop),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                         "frac": achieved / peak, "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS,
+                         "traffic": ncu_traffic(args.config),
                          "kernel": f"k_eval<{cfg.problem}>", "kernel_ms": k_avg_ms,
                          "bytes_per_launch": bytes_launch, "peak_source": peak_src},
             "clocks": clk,
@@ -325,6 +368,9 @@ def _sample_rows(cfg, cores, seconds):
 
 
 def run_reference(args, cfg, rank):
+    """The reference arm: the CPU oracle, as it stands, timed per generation on a bounded row
+    sample of the same workload (this tier has no installable reference implementation);
+    the line's `config` is the GPU arm's, the sample is stated in cpu_baseline.sample."""
     if rank != 0:
         return
     cores = os.cpu_count() or 1
@@ -346,11 +392,11 @@ def run_reference(args, cfg, rank):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t * 1e3 * cfg.pop / rows, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg.note, "algo": cfg.algo, "problem": cfg.problem,
-                       "pop": cfg.pop, "dim": cfg.dim},
+            "config": config_dict(cfg, args.gpus, args.exchange),
             "individual_dims_per_s": value * cfg.pop * D * (0.5 if cfg.algo == "cso" else 1),
             "cpu_baseline": {"value": value, "unit": _unit(cfg), "cores": cores,
-                             "kind": "oracle", "sample": sample},
+                             "kind": "oracle", "sample": sample, "cpu_model": cpu_model(),
+                             "nproc": cores},
             "e2e": {"value": value, "unit": _unit(cfg), "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -461,6 +507,8 @@ def main():
     # ---- timed region: K generations, device-timed with CUDA events on the handle's stream
     h.set_timing(True)               # events around every generation kernel (dominant kernel)
     h.kernel_time(reset=True)
+    if cfg.algo == "pso":
+        h.fin_time(reset=True)
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -473,12 +521,14 @@ def main():
     clk = clocks.stop()
     ms_local = e0.elapsed_time(e1)
     k_ms, k_n, k_launch = h.kernel_time(reset=True)
+    fin_ms, fin_launch = h.fin_time(reset=True) if cfg.algo == "pso" else (0.0, 0)
     h.set_timing(False)
     # one launch of the persistent small-population kernel runs all the steps
-    t = torch.tensor([ms_local, k_ms / max(k_n, 1)], dtype=torch.float64, device=cdev)
+    t = torch.tensor([ms_local, k_ms / max(k_n, 1), fin_ms / max(fin_launch, 1)],
+                     dtype=torch.float64, device=cdev)
     if launched:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total, k_avg_ms = float(t[0]), float(t[1])
+    ms_total, k_avg_ms, fin_avg_ms = float(t[0]), float(t[1]), float(t[2])
     ms_per_step = ms_total / args.steps
 
     # ---- end to end: one whole job through the public API with host buffers, timed by the
@@ -490,15 +540,22 @@ def main():
     t0 = time.perf_counter()
     h = open_handle()
     h.step(cfg.problem, 0)
+    h.sync()
+    t_setup = time.perf_counter()
+    t_best = 0.0
     for _ in range(args.e2e_steps):
         h.step(cfg.problem, 1)
-        best = h.best(with_row=True)
+        tb = time.perf_counter()
+        best = h.best(with_row=True)  # synchronising: waits for the step, then D2H
+        t_best += time.perf_counter() - tb
+    t_steps = time.perf_counter()
     hist = h.history()
     e2e_s = time.perf_counter() - t0
-    e2e = torch.tensor([e2e_s], dtype=torch.float64, device=cdev)
+    parts = [e2e_s, t_setup - t0, t_steps - t_setup, t_best, e2e_s - (t_steps - t0)]
+    e2e = torch.tensor(parts, dtype=torch.float64, device=cdev)
     if launched:
         dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
-    e2e_s = float(e2e[0])
+    e2e_s, setup_s, steps_s, best_s, hist_s = (float(v) for v in e2e)
     e2e_h2d = 2 * 4 * cfg.dim / args.e2e_steps            # lb, ub (per job, amortised)
     e2e_d2h = (4 + 8 + 4 * cfg.dim) + 4 * len(hist) / args.e2e_steps
 
@@ -524,28 +581,37 @@ def main():
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": cfg.note, "algo": cfg.algo, "problem": cfg.problem,
-                       "pop": cfg.pop, "dim": cfg.dim, "seed": 0,
-                       "parallelism": f"row-sharded x{world}" + (
-                           f", exchange={'peer-memory (in-kernel)' if peer else ('peer-memory donors' if cfg.algo == 'de' else ('peer-memory pairs' if cso_peer else 'nccl'))}"
-                           if world > 1 else ""),
-                       "l2": "state (X,V,P) > L2: inputs larger than L2, no flush needed"
-                       if 12 * cfg.pop * cfg.dim > 2 * 126e6 else "state comparable to L2"},
+            "config": config_dict(cfg, world, args.exchange),
             "individual_dims_per_s": gens_per_s * evaluated,
             "bytes_per_generation": algorithmic_bytes(cfg, cfg.pop),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS,
+                         "traffic": traffic,
                          "kernel": kname,
                          "kernel_ms": k_avg_ms, "bytes_per_launch": bytes_launch,
                          "peak_source": peak_src},
             "clocks": clk,
             "device": _device_info(local),
-            # generation kernels timed by the library (+ the gbest select per step when W > 1)
-            "gpu_launches": k_launch + (args.steps if (cfg.algo == "pso" and world > 1
-                                                       and not peer) else 0),
+            # generation kernels timed by the library, the gbest-publication / key-first
+            # exchange kernel k_pso_fin when it runs (wave grid, W > 1 peer exchange), and the
+            # gbest select per step of the NCCL exchange
+            "gpu_launches": k_launch + fin_launch + (args.steps if (cfg.algo == "pso" and world > 1
+                                                                    and not peer) else 0),
+            "exchange": ({"kernel": "k_pso_fin", "ms_per_gen": fin_avg_ms,
+                          "frac_of_step": fin_avg_ms / ms_per_step,
+                          "what": ("key-first peer exchange (8-byte keys to every rank; the "
+                                   "winner row pulled over NVLink on a strict improvement) + "
+                                   "gbest publication" if peer else
+                                   "gbest publication after the wave-grid generation kernel")}
+                         if fin_launch else None),
             "e2e": {"value": args.e2e_steps / e2e_s, "unit": "generations/s",
                     "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
                     "steps": args.e2e_steps,
+                    "breakdown_ms": {"setup": setup_s * 1e3,
+                                     "per_step": steps_s * 1e3 / args.e2e_steps,
+                                     "per_step_best_call": best_s * 1e3 / args.e2e_steps,
+                                     "history": hist_s * 1e3,
+                                     "device_step": ms_per_step},
                     "note": "host clock over one whole job through the C-ABI: init from host "
                             "lb/ub (H2D; the population is the method's own Philox init from "
                             "the seed, R-3), generation 0, then per step evox_*_step(1) + "

@@ -225,15 +225,23 @@ evox_status evox_pso_sync(evox_pso* s);
 evox_status evox_pso_set_timing(evox_pso* s, int enable);
 evox_status evox_pso_kernel_time(evox_pso* s, double* total_ms, int64_t* gens, int64_t* launches,
                                  int reset);
+/* The same for the gbest-publication kernel k_pso_fin, which follows the generation kernel
+ * when the exchange is the in-kernel peer exchange (world > 1) or the population runs on
+ * the wave grid: its summed device time (the key-first exchange, the staged / pulled winner
+ * row, G) and launch count since the last reset.  Synchronising. */
+evox_status evox_pso_fin_time(evox_pso* s, double* total_ms, int64_t* launches, int reset);
 
 /* In-kernel peer-memory exchange (the paper's per-
- * iteration all-gather, fused into the generation kernel).  Every
- * handle owns a device "mailbox" of 2 x world slots {u64 flag; u64 key;
- * f32 row[ld]}.  Once connected, the last CTA of each rank's generation
- * kernel writes its winner record into slot[gen parity][rank] of EVERY rank's
- * mailbox (NVLink peer stores), release-publishes the flag, waits for the
- * world records of that generation in its own mailbox, and applies the
- * strict gbest selection itself -- no NCCL launch, no select kernel.
+ * iteration all-gather, done on the device right after each
+ * generation kernel by the gbest-publication kernel, with no host involvement).
+ * Every handle owns a device "mailbox" of 2 x world slots {u64 flag; u64 key;
+ * f32 row[ld]}.  KEY FIRST: a rank whose local minimum can still improve gbest
+ * stages that row in its OWN slot[gen parity][rank]; every rank writes only its
+ * 8-byte key and a release flag into slot[parity][rank] of EVERY rank's mailbox
+ * (NVLink peer stores), waits for the world keys in its own mailbox, picks the
+ * minimum (lowest global index on ties) and, on a strict improvement, pulls that
+ * one row from the winner's mailbox into its gbest -- no NCCL launch, no select
+ * kernel, one row over NVLink per rank per improving generation.
  *
  * evox_pso_mailbox: this handle's mailbox (device pointer and size).
  * evox_pso_mailbox_ipc: its cudaIpcMemHandle (64 bytes) for other processes.

@@ -83,15 +83,18 @@ struct Base {
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending, ev_free;
     std::vector<int64_t> ev_gens;
+    std::vector<int> ev_slot;    // 0: generation kernel, 1: gbest publication / exchange
     double kernel_ms = 0.0;
     int64_t kernel_n = 0;        // generations run by the timed launches
     int64_t kernel_launches = 0;
+    double fin_ms = 0.0;         // k_pso_fin (gbest publication + key-first exchange)
+    int64_t fin_launches = 0;
 };
 
 // Timed launch: events around the kernel enqueued by `launch`, which runs
 // `gens` generations.
 template <class F>
-cudaError_t timed(Base* b, F launch, int64_t gens = 1) {
+cudaError_t timed(Base* b, F launch, int64_t gens = 1, int slot = 0) {
     if (!b->timing) return launch();
     std::pair<cudaEvent_t, cudaEvent_t> ev;
     if (!b->ev_free.empty()) {
@@ -107,6 +110,7 @@ cudaError_t timed(Base* b, F launch, int64_t gens = 1) {
     if (e == cudaSuccess) e = cudaEventRecord(ev.second, b->stream);
     b->ev_pending.push_back(ev);
     b->ev_gens.push_back(gens);
+    b->ev_slot.push_back(slot);
     return e;
 }
 
@@ -117,13 +121,19 @@ cudaError_t collect_timing(Base* b) {
         float ms = 0.0f;
         cudaError_t e = cudaEventElapsedTime(&ms, ev.first, ev.second);
         if (e != cudaSuccess) return e;
-        b->kernel_ms += ms;
-        b->kernel_n += b->ev_gens[i];
-        b->kernel_launches += 1;
+        if (b->ev_slot[i] == 1) {
+            b->fin_ms += ms;
+            b->fin_launches += 1;
+        } else {
+            b->kernel_ms += ms;
+            b->kernel_n += b->ev_gens[i];
+            b->kernel_launches += 1;
+        }
         b->ev_free.push_back(ev);
     }
     b->ev_pending.clear();
     b->ev_gens.clear();
+    b->ev_slot.clear();
     return cudaSuccess;
 }
 
@@ -446,6 +456,7 @@ struct evox_pso : Base {
     unsigned char* rec = nullptr;
     int64_t rec_stride = 0;
     int gen_grid[5] = {0, 0, 0, 0, 0};
+    bool wave = false;  // big population on the wave grid (k_pso_gen_wave + k_pso_fin)
     // in-kernel peer exchange (evox_pso_connect)
     unsigned char* mbox = nullptr;  // own mailbox (separate cudaMalloc: IPC-exportable)
     size_t mb_bytes = 0;
@@ -477,6 +488,7 @@ struct evox_pso : Base {
         a.world = world;
         a.exchange = comm != nullptr && !peer;
         a.peer = peer ? 1 : 0;
+        a.fin_kernel = (peer || wave) ? 1 : 0;
         a.mb_slot = mb_slot;
         a.peer_timeout_ns = peer_timeout_ns;
         for (int r = 0; r < evox::kMaxPeers; ++r) a.mbox[r] = peers[r];
@@ -659,6 +671,7 @@ evox_status evox_pso_init(int64_t pop, int64_t dim, const float* lb, const float
         if (e != cudaSuccess) st = poison(s, EVOX_ERR_CUDA, "pso init", e);
         for (int p = 0; p < 5 && st == EVOX_OK; ++p)
             s->gen_grid[p] = evox::pso_gen_grid(p, s->ld, s->rows, s->device, pso_use_wave(s));
+        s->wave = pso_use_wave(s);
     }
     if (st != EVOX_OK) {
         std::string keep = t_err;
@@ -713,7 +726,9 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
     st = run_graphed(s, (int)problem, n_gens, [&]() -> evox_status {
         CU(s, timed(s, [&] { return evox::launch_pso_gen((int)problem, a, grid, s->stream,
                                                       (s->flags & EVOX_FLAG_TMA) != 0,
-                                                      pso_use_wave(s)); }));
+                                                      s->wave); }));
+        if (a.fin_kernel)
+            CU(s, timed(s, [&] { return evox::launch_pso_fin(a, -1, s->stream); }, 0, 1));
         return pso_exchange(s);
     });
     if (st != EVOX_OK) return st;
@@ -1040,6 +1055,22 @@ evox_status evox_pso_kernel_time(evox_pso* s, double* total_ms, int64_t* gens, i
         s->kernel_ms = 0.0;
         s->kernel_n = 0;
         s->kernel_launches = 0;
+    }
+    return EVOX_OK;
+}
+
+evox_status evox_pso_fin_time(evox_pso* s, double* total_ms, int64_t* launches, int reset) {
+    evox_status st = check_pso(s);
+    if (st != EVOX_OK) return st;
+    st = sync_check(s);
+    if (st != EVOX_OK) return st;
+    DevGuard g(s->device);
+    CU(s, collect_timing(s));
+    if (total_ms) *total_ms = s->fin_ms;
+    if (launches) *launches = s->fin_launches;
+    if (reset) {
+        s->fin_ms = 0.0;
+        s->fin_launches = 0;
     }
     return EVOX_OK;
 }

@@ -26,6 +26,9 @@ struct Ctl {
     unsigned long long* hkeys;   // CSO, world > 1: per-generation local min keys
     unsigned long long hist_cap;
     unsigned long long min_key;  // DE with peers: global min key of the current population
+    unsigned int fin_cnt;        // k_pso_fin: CTAs that staged their slice (reset by CTA 0)
+    unsigned int fin_epoch;      // k_pso_fin: t_new + 1 once CTA 0 has decided the exchange
+    int fin_sel;                 // k_pso_fin: rank whose staged row becomes gbest (-1: none)
 };
 
 // One rank's PSO state, as seen by kernels.
@@ -53,6 +56,7 @@ struct PsoArgs {
     int rank, world;
     int exchange;  // 1: publish the local winner record for the NCCL exchange (A13)
     int peer;      // 1: in-kernel peer-memory exchange through the mailboxes
+    int fin_kernel;  // 1: the gbest publication / exchange runs in k_pso_fin after the kernel
     long long mb_slot;            // bytes per mailbox slot (16 + 4 ld, 16-aligned)
     unsigned long long peer_timeout_ns;
     unsigned char* mbox[kMaxPeers];  // every rank's mailbox (own included)
@@ -129,6 +133,9 @@ cudaError_t launch_eval(int problem, const float* X, long long rows, long long D
 // tma: the bulk-copy-staged variant (warp-per-row geometry only; EVOX_FLAG_TMA)
 cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t st, bool tma,
                            bool wave);
+// k_pso_fin: gbest publication (+ key-first peer exchange) after a generation or tell kernel
+// whose PsoArgs.fin_kernel is set; t_new < 0: the index ctl->t + 1.
+cudaError_t launch_pso_fin(const PsoArgs& a, long long t_new, cudaStream_t st);
 // Big populations take the wave grid (k_pso_gen_wave + k_pso_fin) unless no_wave.
 bool pso_wave(long long ld, long long rows);
 // Mode-A next-row L2 prefetch of the PSO generation (PsoArgs.pf_next): a schedule choice

@@ -116,73 +116,6 @@ struct WindowPrefetch {
     }
 };
 
-// The last CTA's winner record -> every rank's mailbox slot[par][rank]; wait for
-// the world records of this generation; strict gbest selection (A13, fused).
-// Every rank selects from the same world records: identical G on all ranks.
-__device__ void peer_exchange(const PsoArgs& a, unsigned long long key, unsigned long long t_new) {
-    __shared__ int sh_w, sh_better;
-    __shared__ unsigned long long sh_key;
-    Ctl* ctl = a.ctl;
-    const long long NQ = a.ld >> 2;
-    const int par = (int)(t_new & 1);
-    const unsigned long long flag = t_new + 1;  // mailboxes start zeroed: 0 = nothing yet
-    const bool any = key != ~0ull;
-    const long long grow = (long long)(uint32_t)(key & 0xffffffffu);
-    const float4* src = reinterpret_cast<const float4*>(a.X + (any ? grow - a.row0 : 0) * a.ld);
-    const long long my_off = ((long long)par * a.world + a.rank) * a.mb_slot;
-    for (long long q = threadIdx.x; q < NQ; q += blockDim.x) {
-        const float4 v = any ? __ldcg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int p = 0; p < a.world; ++p)
-            reinterpret_cast<float4*>(a.mbox[p] + my_off + 16)[q] = v;
-    }
-    if (threadIdx.x == 0)
-        for (int p = 0; p < a.world; ++p)
-            *reinterpret_cast<unsigned long long*>(a.mbox[p] + my_off + 8) = key;
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int p = 0; p < a.world; ++p)
-            st_release_sys(reinterpret_cast<unsigned long long*>(a.mbox[p] + my_off), flag);
-        // wait for every rank's record of this generation in our own mailbox
-        const unsigned long long t0 = globaltimer_ns();
-        unsigned long long kmin = ~0ull;
-        int w = -1;
-        for (int r = 0; r < a.world; ++r) {
-            const unsigned char* slot = a.mbox[a.rank] + ((long long)par * a.world + r) * a.mb_slot;
-            while (ld_acquire_sys(reinterpret_cast<const unsigned long long*>(slot)) != flag) {
-                if (globaltimer_ns() - t0 > a.peer_timeout_ns) {
-                    ctl->err = 1;
-                    break;
-                }
-                __nanosleep(256);
-            }
-            const unsigned long long kr = __ldcg(reinterpret_cast<const unsigned long long*>(slot + 8));
-            if (kr < kmin) { kmin = kr; w = r; }
-        }
-        const bool ok = kmin != ~0ull;
-        const float fmin = ok ? unord_f32((uint32_t)(kmin >> 32)) : __int_as_float(0x7f800000);
-        sh_key = kmin;
-        sh_w = w;
-        sh_better = ok && fmin < ctl->gf;  // strict improvement (R-5)
-    }
-    __syncthreads();
-    if (sh_better) {
-        const float4* wr = reinterpret_cast<const float4*>(
-            a.mbox[a.rank] + ((long long)par * a.world + sh_w) * a.mb_slot + 16);
-        float4* G = reinterpret_cast<float4*>(a.G);
-        for (long long q = threadIdx.x; q < NQ; q += blockDim.x) G[q] = __ldcg(wr + q);
-    }
-    if (threadIdx.x == 0) {
-        const unsigned long long k = sh_key;
-        const float fmin = k != ~0ull ? unord_f32((uint32_t)(k >> 32)) : __int_as_float(0x7f800000);
-        if (sh_better) {
-            ctl->gf = fmin;
-            ctl->gidx = (long long)(uint32_t)(k & 0xffffffffu);
-        }
-        ctl->hist[t_new] = fmin;
-    }
-}
-
 // In the last CTA: gbest update (strict, R-5), hist, or the winner record for
 // the exchange.  `t_new` is the index of the population just evaluated.
 __device__ void pso_finalize(const PsoArgs& a, unsigned long long key, unsigned long long t_new) {
@@ -191,9 +124,7 @@ __device__ void pso_finalize(const PsoArgs& a, unsigned long long key, unsigned 
     const bool any = key != ~0ull;
     const long long grow = (long long)(uint32_t)(key & 0xffffffffu);
     const float fmin = any ? unord_f32((uint32_t)(key >> 32)) : __int_as_float(0x7f800000);
-    if (a.peer) {
-        peer_exchange(a, key, t_new);
-    } else if (a.exchange) {
+    if (a.exchange) {
         // winner record {u64 key; u32 pad[2]; f32 row[ld]} into this rank's slot
         unsigned char* rec = a.rec + (long long)a.rank * a.rec_stride;
         const float4* src = reinterpret_cast<const float4*>(a.X + (any ? grow - a.row0 : 0) * a.ld);
@@ -330,7 +261,7 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : (G::LPR == 4
     const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
     const unsigned long long best = pso_gen_rows<P, G, UNI, false>(a, m, t, htab, sh_acc, sh_head);
     unsigned long long key;
-    if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
+    if (grid_argmin(a.ctl, best, &key) && !a.fin_kernel) pso_finalize(a, key, t + 1);
 }
 
 #ifndef EVOX_WAVE_MINB
@@ -395,14 +326,144 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : EVOX_WAVE_MI
     }
 }
 
-// gbest publication of a wave generation (one CTA): the last-CTA step of k_pso_gen --
-// strict improvement, hist, t; or the winner record / peer exchange for world > 1.
-__global__ void __launch_bounds__(256) k_pso_fin(PsoArgs a) {
+// Copy `n` quads src -> dst with this grid's threads, 4 float4 loads in flight per thread.
+__device__ __forceinline__ void grid_copy4(float4* dst, const float4* src, long long n) {
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; q + 3 * nth < n; q += 4 * nth) {
+        const float4 v0 = __ldcg(src + q), v1 = __ldcg(src + q + nth);
+        const float4 v2 = __ldcg(src + q + 2 * nth), v3 = __ldcg(src + q + 3 * nth);
+        dst[q] = v0;
+        dst[q + nth] = v1;
+        dst[q + 2 * nth] = v2;
+        dst[q + 3 * nth] = v3;
+    }
+    for (; q < n; q += nth) dst[q] = __ldcg(src + q);
+}
+
+// gbest publication after a generation (or tell) kernel that only reduced the generation's
+// minimum key into ctl->gen_key (PsoArgs.fin_kernel): the last-CTA step of k_pso_gen, run by
+// a small grid so the row copies are spread over several SMs.
+//  * one rank: strict improvement -> G <- X[i*], gf, gidx; hist; t.
+//  * NCCL exchange: this rank's winner record {key; row} for the all-gather.
+//  * peer exchange, KEY FIRST (A13; the paper's per-iteration all-gather of fitness,
+//    P:583-587): a rank whose local minimum can still improve gbest stages its row in its
+//    OWN mailbox slot[par][rank] (local copy); every rank then writes only its 8-byte key +
+//    release flag into every rank's mailbox; each rank picks the minimum key (lowest global
+//    index on ties, R-11) and, on a strict improvement over gf, pulls that ONE row from the
+//    winner's mailbox over NVLink into G.  One row crosses NVLink per rank per improving
+//    generation (was: W rows pushed per rank every generation).  Parity double-buffering:
+//    a rank overwrites slot[par] only at t_new + 2, after every peer published t_new + 1,
+//    i.e. finished this pull (stream order).  Bounded waits (ctl->err, no hang).
+__global__ void __launch_bounds__(256) k_pso_fin(PsoArgs a, long long t_arg) {
+    __shared__ int sh_sel;
     pdl_wait();
     pdl_launch_dependents();
-    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
-    const unsigned long long key = *(volatile unsigned long long*)&a.ctl->gen_key;
-    pso_finalize(a, key, t + 1);
+    Ctl* ctl = a.ctl;
+    // every CTA reads the control block BEFORE CTA 0 rewrites it (arrival counter below)
+    const unsigned long long t_new =
+        t_arg >= 0 ? (unsigned long long)t_arg : *(volatile unsigned long long*)&ctl->t + 1;
+    const unsigned long long key = *(volatile unsigned long long*)&ctl->gen_key;
+    const float gf_old = *(volatile float*)&ctl->gf;
+    const long long NQ = a.ld >> 2;
+    const bool any = key != ~0ull;
+    const long long grow = (long long)(uint32_t)(key & 0xffffffffu);
+    const float fmin = any ? unord_f32((uint32_t)(key >> 32)) : __int_as_float(0x7f800000);
+    const float4* xrow = reinterpret_cast<const float4*>(a.X + (any ? grow - a.row0 : 0) * a.ld);
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    const int par = (int)(t_new & 1);
+    const unsigned long long flag = t_new + 1;  // mailboxes start zeroed: 0 = nothing yet
+    const long long my_off = ((long long)par * a.world + a.rank) * a.mb_slot;
+    if (a.peer) {  // 1. a possible winner stages its row in its own mailbox (local HBM)
+        if (any && fmin < gf_old)
+            grid_copy4(reinterpret_cast<float4*>(a.mbox[a.rank] + my_off + 16), xrow, NQ);
+    } else if (a.exchange) {  // NCCL: winner record {u64 key; pad; f32 row[ld]} of this rank
+        unsigned char* rec = a.rec + (long long)a.rank * a.rec_stride;
+        if (any) {
+            grid_copy4(reinterpret_cast<float4*>(rec + 16), xrow, NQ);
+        } else {
+            for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < NQ;
+                 q += (long long)gridDim.x * blockDim.x)
+                reinterpret_cast<float4*>(rec + 16)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (lead) *reinterpret_cast<unsigned long long*>(rec) = key;
+    } else if (any && fmin < gf_old) {  // one rank: strict improvement (R-5)
+        grid_copy4(reinterpret_cast<float4*>(a.G), xrow, NQ);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (a.peer) __threadfence_system();
+        atomicAdd(&ctl->fin_cnt, 1u);
+    }
+    if (!lead && !a.peer) return;
+    unsigned long long t0 = 0;
+    if (lead) {
+        t0 = globaltimer_ns();
+        while (ld_acquire_gpu_u32(&ctl->fin_cnt) != gridDim.x) {  // every CTA has read ctl
+            if (globaltimer_ns() - t0 > a.peer_timeout_ns) { ctl->err = 1; break; }
+            __nanosleep(64);
+        }
+        ctl->fin_cnt = 0u;
+        ctl->gen_key = ~0ull;
+        ctl->ticket = 0u;
+        ctl->t = t_new;
+        if (!a.peer) {
+            if (!a.exchange) {
+                if (any && fmin < gf_old) {
+                    ctl->gf = fmin;
+                    ctl->gidx = grow;
+                }
+                ctl->hist[t_new] = fmin;
+            }
+            return;
+        }
+        // 2. the 8-byte key into every rank's slot, then the release flags
+        for (int p = 0; p < a.world; ++p)
+            *reinterpret_cast<unsigned long long*>(a.mbox[p] + my_off + 8) = key;
+        __threadfence_system();
+        for (int p = 0; p < a.world; ++p)
+            st_release_sys(reinterpret_cast<unsigned long long*>(a.mbox[p] + my_off), flag);
+        // 3. every rank's key of this generation, from our own mailbox
+        unsigned long long kmin = ~0ull;
+        int w = -1;
+        for (int r = 0; r < a.world; ++r) {
+            const unsigned char* slot =
+                a.mbox[a.rank] + ((long long)par * a.world + r) * a.mb_slot;
+            while (ld_acquire_sys(reinterpret_cast<const unsigned long long*>(slot)) != flag) {
+                if (globaltimer_ns() - t0 > a.peer_timeout_ns) { ctl->err = 1; break; }
+                __nanosleep(128);
+            }
+            const unsigned long long kr =
+                __ldcg(reinterpret_cast<const unsigned long long*>(slot + 8));
+            if (kr < kmin) { kmin = kr; w = r; }
+        }
+        const bool ok = kmin != ~0ull;
+        const float gmin = ok ? unord_f32((uint32_t)(kmin >> 32)) : __int_as_float(0x7f800000);
+        const bool better = ok && gmin < gf_old;  // strict improvement (R-5)
+        if (better) {
+            ctl->gf = gmin;
+            ctl->gidx = (long long)(uint32_t)(kmin & 0xffffffffu);
+        }
+        ctl->hist[t_new] = gmin;
+        ctl->fin_sel = better ? w : -1;
+        __threadfence();
+        st_release_gpu_u32(&ctl->fin_epoch, (unsigned int)flag);
+    }
+    // 4. every CTA: the decision, then its slice of the winner's staged row -> G
+    if (threadIdx.x == 0) {
+        t0 = globaltimer_ns();
+        while (ld_acquire_gpu_u32(&ctl->fin_epoch) != (unsigned int)flag) {
+            if (globaltimer_ns() - t0 > 2 * a.peer_timeout_ns) { ctl->err = 1; break; }
+            __nanosleep(64);
+        }
+        sh_sel = *(volatile int*)&ctl->fin_sel;
+    }
+    __syncthreads();
+    if (sh_sel >= 0)
+        grid_copy4(reinterpret_cast<float4*>(a.G),
+                   reinterpret_cast<const float4*>(a.mbox[sh_sel] +
+                                                   ((long long)par * a.world + sh_sel) * a.mb_slot + 16),
+                   NQ);
 }
 
 #ifndef EVOX_MID_PF
@@ -749,7 +810,7 @@ __global__ void __launch_bounds__(256, EVOX_MINB) k_pso_gen_tma(PsoArgs a) {
         }
     }
     unsigned long long key;
-    if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t + 1);
+    if (grid_argmin(a.ctl, best, &key) && !a.fin_kernel) pso_finalize(a, key, t + 1);
 }
 
 // Unfused ask: move X_t -> X_{t+1} (no evaluation).
@@ -793,7 +854,7 @@ __global__ void __launch_bounds__(256) k_pso_tell(PsoArgs a, const float* __rest
         best = k < best ? k : best;
     }
     unsigned long long key;
-    if (grid_argmin(a.ctl, best, &key)) pso_finalize(a, key, t);
+    if (grid_argmin(a.ctl, best, &key) && !a.fin_kernel) pso_finalize(a, key, t);
 }
 
 // world > 1: after the all-gather of the W winner records, pick the min key
@@ -919,7 +980,6 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
             using GW_ = Geom<G_::LPR, G_::WPR, G_::WPR == 1 ? EVOX_WAVE_U : G_::NU, G_::EFL>;
             e = launch_pdl(k_pso_gen_wave<P_, GW_, U_>, grid, a, st);
         })));
-        if (e == cudaSuccess) e = launch_pdl(k_pso_fin, 1, a, st);
         return e != cudaSuccess ? e : cudaGetLastError();
     }
     if (use_tma(a.ld, tma)) {
@@ -979,7 +1039,28 @@ cudaError_t launch_pso_tell(const PsoArgs& a, const float* fit, unsigned long lo
     cudaGetDevice(&dev);
     const int g = grid_for((const void*)k_pso_tell, (a.rows + 255) / 256, dev);
     k_pso_tell<<<g, 256, 0, st>>>(a, fit, t);
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && a.fin_kernel) e = launch_pso_fin(a, (long long)t, st);
+    return e;
+}
+
+// One CTA per 16 KB of the row (at most 64): the staged / pulled rows are copied by a few
+// SMs, so even a 400 KB row (C5) moves in a few microseconds.
+cudaError_t launch_pso_fin(const PsoArgs& a, long long t_new, cudaStream_t st) {
+    long long g = (a.ld * 4 + 16383) / 16384;
+    if (g > 64) g = 64;
+    if (g < 1) g = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)g);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pso_fin, a, t_new);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_gbest_select(const PsoArgs& a, cudaStream_t st) {

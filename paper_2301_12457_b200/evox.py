@@ -101,6 +101,7 @@ SIGNATURES = {
     "evox_pso_mailbox_ipc": ([_p, _p], _i),
     "evox_pso_connect": ([_p, _i, _p], _i),
     "evox_pso_kernel_time": ([_p, ctypes.POINTER(ctypes.c_double), _PI64, _PI64, _i], _i),
+    "evox_pso_fin_time": ([_p, ctypes.POINTER(ctypes.c_double), _PI64, _i], _i),
     "evox_cso_workspace_bytes": ([_i64, _i64, _i, _i, _PSZ], _i),
     "evox_cso_init": ([_i64, _i64, _p, _p, _f32, _i64, _u64, _p, _PP], _i),
     "evox_cso_step": ([_p, _i, _i64], _i),
@@ -427,6 +428,12 @@ class PSO(_Handle):
         """Multi-process group: `handles` = [64-byte PSO.mailbox_ipc() of rank r]."""
         buf = ctypes.create_string_buffer(b"".join(bytes(h) for h in handles))
         _check(lib().evox_pso_connect(self._h, 1, buf))
+
+    def fin_time(self, reset: bool = False) -> tuple[float, int]:
+        """(summed device time in ms of the gbest-publication / exchange kernel, launches)."""
+        ms, k = ctypes.c_double(), ctypes.c_int64()
+        _check(lib().evox_pso_fin_time(self._h, ctypes.byref(ms), ctypes.byref(k), int(reset)))
+        return ms.value, k.value
 
     def tell(self, fitness):
         """Algorithm.tell with a [rows] float32 CUDA tensor of this rank's fitness."""

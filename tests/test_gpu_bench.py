@@ -16,15 +16,15 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("config", ["H", "C3", "D1"])
-def test_bench_two_ranks_same_gpu(config):
+@pytest.mark.parametrize("config,pop", [("H", 20000), ("C3", 20000), ("D1", 20000), ("C5", 400)])
+def test_bench_two_ranks_same_gpu(config, pop):
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     env = dict(os.environ, EVOX_BENCH_SAME_GPU="1")
     nproc = 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + random.randrange(300)),
-           "bench.py", "--gpus", str(nproc), "--config", config, "--pop", "20000", "--steps", "3",
+           "bench.py", "--gpus", str(nproc), "--config", config, "--pop", str(pop), "--steps", "3",
            "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
@@ -33,7 +33,10 @@ def test_bench_two_ranks_same_gpu(config):
     d = json.loads(lines[0])
     assert d["n_gpus"] == nproc and d["steps"] == 3 and d["value"] > 0
     assert d["roofline"]["bound"] == "hbm" and d["gpu_launches"] >= 3
-    assert d["config"]["pop"] == 20000
+    assert d["config"]["pop"] == pop
+    if config in ("H", "C5"):  # the key-first peer exchange kernel runs once per generation
+        assert d["exchange"]["kernel"] == "k_pso_fin" and d["exchange"]["ms_per_gen"] > 0
+        assert d["gpu_launches"] >= 6
 
 
 @pytest.mark.parametrize("config", ["EH-rosenbrock", "E5-griewank"])
