@@ -995,7 +995,10 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-bool pso_small(long long rows, long long ld) { return rows * ld <= 65536; }
+// One CTA walking the whole population beats the resident cooperative grid (~11 us per
+// generation at any small size) only below ~2^14 elements: pop 100 x dim 128 8.9 us, x 512
+// 29 us per generation in one CTA (profiles/r02_sweeps.txt); C1 (100 x 10) stays here.
+bool pso_small(long long rows, long long ld) { return rows * ld <= 16384; }
 
 // Mid-size populations run n generations in one cooperative launch (k_pso_run_mid);
 // beyond 2^25 elements a generation is long enough that the launch cost is noise.
