@@ -1,3 +1,5 @@
+# same-box A/B of measurement builds in paper_2301_12457_b200/variants/ (built by
+# scripts/var_build.sh): bash scripts/gpu_ab.sh "<configs>" "<base|variant names>" [reps]
 # same-box A/B of library variants: bash scripts/gpu_r02_ab.sh "<configs>" "<variants>" [reps]
 out=gpurun_out/r02_ab.txt; : > $out
 for rep in $(seq 1 ${3:-1}); do

@@ -1,11 +1,14 @@
-#!/bin/bash
-# One GPU round: parity tests, smoke, bench, ncu launch list + full capture of the top kernel.
-# Usage (from the repo root, under gpurun): bash scripts/gpu_check.sh [quick]
-mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 1500 python -m pytest tests -m gpu -q -rA --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
-echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-[ "$1" == "quick" ] && exit 0
-timeout 600 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_H.json 2> gpurun_out/bench_H.err
-echo "bench rc=$?" >> gpurun_out/bench_H.err
+# round-2 GPU check: the whole -m gpu suite, bench lines, and the 2-rank same-GPU flow
+timeout 1500 python -m pytest tests -m gpu -q -x --durations=10 > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+tail -15 gpurun_out/pytest_gpu.log
+for c in H C5 C4g; do python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 20 > gpurun_out/b_$c.json 2>gpurun_out/b_$c.err; done
+for c in H C5; do EVOX_BENCH_SAME_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --config $c --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/b2_$c.json 2>gpurun_out/b2_$c.err; done
+python - <<'P'
+import json
+for f in ["b_H", "b_C5", "b_C4g", "b2_H", "b2_C5"]:
+    try:
+        d = json.loads([l for l in open(f"gpurun_out/{f}.json") if l.startswith("{")][-1])
+        print(f, round(d["value"], 2), round(d["roofline"]["frac"], 4), d["roofline"]["kernel"], d.get("exchange"), d["e2e"].get("breakdown_ms"))
+    except Exception as e:
+        print(f, "ERR", e)
+P
