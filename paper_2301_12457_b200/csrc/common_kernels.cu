@@ -75,6 +75,26 @@ __global__ void __launch_bounds__(1024) k_argmin_rows(const float* f, long long 
     }
 }
 
+// best() of one rank's CSO / DE population: the row of the current generation's minimum key
+// (ctl->min_key, written by the generation kernel's finalize), from the buffer its selection
+// flag names (DE: sel[t & 1]; CSO: one buffer), into out [ld].  Nothing if there is no key.
+__global__ void __launch_bounds__(256) k_best_row(const Ctl* ctl, const float* X0, const float* X1,
+                                                  const unsigned char* sel0,
+                                                  const unsigned char* sel1, long long row0,
+                                                  long long rows, long long ld, float* out) {
+    const unsigned long long key = ctl->min_key;
+    if (key == ~0ull) return;
+    const long long r = (long long)(uint32_t)(key & 0xffffffffu) - row0;
+    if (r < 0 || r >= rows) return;
+    const unsigned char* sel = (ctl->t & 1) ? sel1 : sel0;
+    const float* src = (sel != nullptr && sel[r]) ? X1 : X0;
+    const float4* s4 = reinterpret_cast<const float4*>(src + r * ld);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < (ld >> 2);
+         q += (long long)gridDim.x * blockDim.x)
+        o4[q] = s4[q];
+}
+
 __global__ void k_debug_philox(const uint4* ctr, PhiloxKey rk, uint4* out, long long n) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
@@ -135,6 +155,15 @@ cudaError_t launch_eval(int problem, const float* X, long long rows, long long D
 cudaError_t launch_argmin_rows(const float* f, long long rows, long long row0,
                                unsigned long long* key_out, cudaStream_t st) {
     k_argmin_rows<<<1, 1024, 0, st>>>(f, rows, row0, key_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_best_row(const Ctl* ctl, const float* X0, const float* X1,
+                            const unsigned char* sel0, const unsigned char* sel1, long long row0,
+                            long long rows, long long ld, float* out, cudaStream_t st) {
+    long long g = ((ld >> 2) + 255) / 256;
+    if (g > 32) g = 32;
+    k_best_row<<<(int)(g < 1 ? 1 : g), 256, 0, st>>>(ctl, X0, X1, sel0, sel1, row0, rows, ld, out);
     return cudaGetLastError();
 }
 

@@ -71,6 +71,7 @@ struct Base {
     int64_t hist_cap = 0;
     int64_t t = -1;  // index of the current population (-1: not evaluated)
     bool stepped = false;  // a step/ask ran since init or the last load (connect must precede)
+    bool min_key_stale = false;  // CSO/DE: ctl->min_key predates a load (best() recomputes)
     int problem = -1;
     bool poisoned = false;
     ncclComm_t comm = nullptr;
@@ -404,6 +405,56 @@ evox_status base_common_init(Base* b) {
 }
 
 bool valid_problem(int p) { return p >= EVOX_SPHERE && p <= EVOX_ROSENBROCK; }
+
+evox_status ensure_stage(Base* b, size_t need) {
+    if (b->stage_bytes >= need) return EVOX_OK;
+    if (b->stage) cudaFreeHost(b->stage);
+    b->stage = nullptr;
+    b->stage_bytes = 0;
+    CU(b, cudaHostAlloc((void**)&b->stage, need, cudaHostAllocDefault));
+    b->stage_bytes = need;
+    return EVOX_OK;
+}
+
+void decode_key(unsigned long long key, float* fv, int64_t* gi) {
+    *fv = INFINITY;
+    *gi = -1;
+    if (key != ~0ull) {
+        const uint32_t o = (uint32_t)(key >> 32);
+        const uint32_t bits = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+        std::memcpy(fv, &bits, 4);
+        *gi = (int64_t)(uint32_t)(key & 0xffffffffu);
+    }
+}
+
+// best() of a single-rank CSO / DE handle: the generation kernel's finalize already left the
+// population's minimum key in ctl->min_key; one tiny row-gather kernel, two async D2H copies
+// into pinned staging and ONE synchronisation (no population-wide argmin).
+evox_status staged_best(Base* b, const float* X0, const float* X1, const unsigned char* sel0,
+                        const unsigned char* sel1, float* fit, int64_t* global_index,
+                        float* row_host) {
+    const size_t row_bytes = sizeof(float) * (size_t)b->dim;
+    evox_status st = ensure_stage(b, sizeof(Ctl) + sizeof(float) * (size_t)b->ld);
+    if (st != EVOX_OK) return st;
+    if (row_host)
+        CU(b, evox::launch_best_row(b->ctl, X0, X1, sel0, sel1, b->row0, b->rows, b->ld,
+                                    b->scratch_row, b->stream));
+    CU(b, cudaMemcpyAsync(b->stage, b->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, b->stream));
+    if (row_host)
+        CU(b, cudaMemcpyAsync(b->stage + sizeof(Ctl), b->scratch_row, row_bytes,
+                              cudaMemcpyDeviceToHost, b->stream));
+    st = sync_check(b, reinterpret_cast<const Ctl*>(b->stage));
+    if (st != EVOX_OK) return st;
+    Ctl c;
+    std::memcpy(&c, b->stage, sizeof c);
+    float fv;
+    int64_t gi;
+    decode_key(c.min_key, &fv, &gi);
+    if (fit) *fit = fv;
+    if (global_index) *global_index = gi;
+    if (row_host && gi >= 0) std::memcpy(row_host, b->stage + sizeof(Ctl), row_bytes);
+    return EVOX_OK;
+}
 
 // Replay `n` generations of `one` (a callable that enqueues one generation)
 // through cached CUDA graphs of up to kChunk generations.
@@ -790,14 +841,8 @@ evox_status evox_pso_best(evox_pso* s, float* fit, int64_t* global_index, float*
     if (st != EVOX_OK) return st;
     DevGuard g(s->device);
     const size_t row_bytes = sizeof(float) * (size_t)s->dim;
-    const size_t need = sizeof(Ctl) + row_bytes;
-    if (s->stage_bytes < need) {
-        if (s->stage) cudaFreeHost(s->stage);
-        s->stage = nullptr;
-        s->stage_bytes = 0;
-        CU(s, cudaHostAlloc((void**)&s->stage, need, cudaHostAllocDefault));
-        s->stage_bytes = need;
-    }
+    st = ensure_stage(s, sizeof(Ctl) + row_bytes);
+    if (st != EVOX_OK) return st;
     CU(s, cudaMemcpyAsync(s->stage, s->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s->stream));
     if (row_host)
         CU(s, cudaMemcpyAsync(s->stage + sizeof(Ctl), s->G, row_bytes, cudaMemcpyDeviceToHost,
@@ -1325,6 +1370,7 @@ evox_status evox_cso_step(evox_cso* s, evox_problem problem, int64_t n_gens) {
         });
         if (st != EVOX_OK) return st;
         s->t += n_gens;
+        s->min_key_stale = false;
     }
     if (s->comm && !s->peer) {  // one min-reduction of this call's per-generation keys
         const int64_t n = s->t - first + 1;
@@ -1353,6 +1399,8 @@ evox_status evox_cso_best(evox_cso* s, float* fit, int64_t* global_index, float*
         return sync_check(s);
     }
     DevGuard g(s->device);
+    if (!s->peer && !s->comm && !s->min_key_stale)
+        return staged_best(s, s->X, s->X, nullptr, nullptr, fit, global_index, row_host);
     const evox::NcclApi* api = (s->comm && !s->peer) ? evox::nccl_api(nullptr) : nullptr;
     if (!s->peer) {
         CU(s, evox::launch_argmin_rows(s->fcur(), s->rows, s->row0, s->keybuf, s->stream));
@@ -1515,6 +1563,7 @@ evox_status evox_cso_load(evox_cso* s, const void* host_blob, size_t size) {
     CU(s, cudaMemcpy(s->ctl, &c, sizeof c, cudaMemcpyHostToDevice));
     s->t = h.t;
     s->problem = (int)h.problem;
+    s->min_key_stale = true;  // ctl->min_key is the pre-load population's
     s->stepped = false;
     return EVOX_OK;
 }
@@ -1809,6 +1858,7 @@ evox_status evox_de_step(evox_de* s, evox_problem problem, int64_t n_gens) {
     });
     if (st != EVOX_OK) return st;
     s->t += n_gens;
+    s->min_key_stale = false;
     return EVOX_OK;
 }
 
@@ -1904,6 +1954,7 @@ evox_status evox_de_load(evox_de* s, const void* host_blob, size_t size) {
     CU(s, cudaMemcpy(s->ctl, &c, sizeof c, cudaMemcpyHostToDevice));
     s->t = h.t;
     s->problem = (int)h.problem;
+    s->min_key_stale = true;  // ctl->min_key is the pre-load population's
     s->stepped = false;
     return EVOX_OK;
 }
@@ -1946,6 +1997,9 @@ evox_status evox_de_best(evox_de* s, float* fit, int64_t* global_index, float* r
         return sync_check(s);
     }
     DevGuard g(s->device);
+    if (!s->peer && !s->min_key_stale)
+        return staged_best(s, s->buf[0], s->buf[1], s->sel[0], s->sel[1], fit, global_index,
+                           row_host);
     const int p = (int)((s->t < 0 ? 0 : s->t) & 1);
     if (!s->peer) CU(s, evox::launch_argmin_rows(s->f[p], s->rows, s->row0, s->scratch_key, s->stream));
     st = sync_check(s);

@@ -161,6 +161,10 @@ cudaError_t launch_cso_colsum(const CsoArgs& a, double scale, cudaStream_t st);
 cudaError_t launch_cso_colmean(const CsoArgs& a, double inv_scale, cudaStream_t st);
 cudaError_t launch_cso_hist_from_keys(const CsoArgs& a, unsigned long long t0, long long n,
                                       cudaStream_t st);
+// best(): the row of ctl->min_key into out (CSO: sel0 = sel1 = NULL).
+cudaError_t launch_best_row(const Ctl* ctl, const float* X0, const float* X1,
+                            const unsigned char* sel0, const unsigned char* sel1, long long row0,
+                            long long rows, long long ld, float* out, cudaStream_t st);
 cudaError_t launch_argmin_rows(const float* f, long long rows, long long row0,
                                unsigned long long* key_out, cudaStream_t st);
 

@@ -358,37 +358,24 @@ int main() {
     cudaMalloc(&s.P, ab);
     const double b5 = 5.0 * ab;
     const int npg = (int)((s.rows + 7) / 8);
-    St2 s2;
-    s2.X = s.X; s2.V = s.V; s2.P = s.P; s2.rows = s.rows; s2.nq = s.nq;
-    cudaMalloc(&s2.G, 16 * s.nq);
-    cudaMalloc(&s2.f, 4 * s.rows);
-    cudaMalloc(&s2.pf, 4 * s.rows);
-    cudaMalloc(&s2.imp, s.rows);
-    cudaMemset((void*)s2.G, 0, 16 * s.nq);
-    cudaMemset(s2.pf, 0, 4 * s.rows);
-    {   // 45 % of rows pending, pseudo-random
-        unsigned char* h = (unsigned char*)malloc(s.rows);
-        unsigned x = 12345;
-        for (long long i = 0; i < s.rows; ++i) { x = x * 1664525u + 1013904223u; h[i] = (x >> 24) < 115; }
-        cudaMemcpy(s2.imp, h, s.rows, cudaMemcpyHostToDevice);
-        free(h);
-    }
     cudaMemset(s.X, 0x3f, ab);
     cudaMemset(s.V, 0, ab);
     cudaMemset(s.P, 0x3f, ab);
-    const double b4 = 4.0 * ab;
     timeit("np1_ph1", k_np<1>, npg, 256, 0, s, b5);
-    timeit2("np2_F8_m1", k_np2<8, 1>, npg, s2, b5);
-    timeit2("np2_F8_m1_ord", k_np2<8, 1, 1>, npg, s2, b5);
-    timeit2("np2_F8_m3_ord", k_np2<8, 3, 1>, npg, s2, b5);
-    timeit2("np2_F15_m2_ord", k_np2<15, 2, 1>, npg, s2, b5);
-    timeit2("np2_F15_m3_ord", k_np2<15, 3, 1>, npg, s2, b5);
-    {   // no row pending: F15 == the whole kernel at 3R2W
-        cudaMemset(s2.imp, 0, s.rows);
-        timeit2("np2_F15_m3_ord_nopend", k_np2<15, 3, 1>, npg, s2, b5);
-        cudaMemset(s2.imp, 1, s.rows);
-        timeit2("np2_F15_m3_ord_allpend", k_np2<15, 3, 1>, npg, s2, b5);
-    }
+    RING(4, 8, 0, 1, 2);
+    RING(4, 8, 1, 1, 2);
+    RING(4, 4, 0, 1, 3);
+    RING(4, 4, 1, 1, 3);
+    RING(8, 8, 0, 1, 2);
+    RING(8, 8, 1, 1, 2);
+    RING(6, 6, 0, 1, 3);
+    RING(6, 6, 1, 1, 3);
+    RING(8, 16, 0, 1, 1);
+    RING(16, 16, 0, 1, 1);
+    RING(12, 12, 0, 1, 1);
+    RING(2, 4, 0, 1, 4);
+    RING(3, 3, 0, 1, 4);
+    const double b4 = 4.0 * ab;
     (void)b4;
     return 0;
 }

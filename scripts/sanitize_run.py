@@ -24,16 +24,33 @@ for D in (10, 100, 1003, 4099):
         de.step(p, 3)
         de.view("X")
         de.best()
-os.environ["EVOX_NO_SMALL"] = "1"
-pso = ev.PSO(300, 1000, -5, 5, seed=2)   # multi-CTA generation kernel + grid argmin
-pso.step("ackley", 3)
+pso = ev.PSO(300, 1000, -5, 5, seed=2, flags=ev.evox.FLAG_NO_SMALL | ev.evox.FLAG_NO_MID)
+pso.step("ackley", 3)                    # multi-CTA generation kernel + grid argmin
 pso.best()
-hs = [ev.PSO(64, 100, -5, 5, seed=3, rank=r, world=2, stream=torch.cuda.Stream()) for r in range(2)]
-boxes = [h.mailbox()[0] for h in hs]
-for h in hs:
-    h.connect_local(boxes)
-for h in hs:
-    h.step("sphere", 3)
-for h in hs:
+pso = ev.PSO(8200, 4100, -5, 5, seed=2)  # > 2^25 elements, CTA-per-row: wave grid + k_pso_fin
+pso.step("rosenbrock", 2)
+pso.best()
+pso.close()
+for D in (100, 20000):                   # peer exchange: key-first k_pso_fin (5 CTAs at 20000)
+    hs = [ev.PSO(64, D, -5, 5, seed=3, rank=r, world=2, stream=torch.cuda.Stream())
+          for r in range(2)]
+    boxes = [h.mailbox()[0] for h in hs]
+    for h in hs:
+        h.connect_local(boxes)
+    for h in hs:
+        h.step("sphere", 3)
+    for h in hs:
+        h.sync()
+    for h in hs:
+        h.best()
+des = [ev.DE(40, 33, -5, 5, seed=3, rank=r, world=2, stream=torch.cuda.Stream()) for r in range(2)]
+bases = [h.state_base() for h in des]
+for h in des:
+    h.connect_local(bases)
+for h in des:
+    h.step("ackley", 2)
+for h in des:
     h.sync()
+for h in des:
+    h.view("X")                          # gathered without touching the peer-read state
 print("sanitize run ok")

@@ -209,3 +209,25 @@ def test_de_save_load_roundtrip():
     c = ev.DE(N, D, -5.12, 5.12, seed=4, CR=0.5)
     with pytest.raises(E.ContractError):
         c.load(blob)
+
+
+@pytest.mark.parametrize("algo", ["de", "cso"])
+def test_best_from_generation_key_and_after_load(algo):
+    """best() of a single-rank CSO / DE reads the minimum key the generation kernel left in the
+    control block (no population argmin): it must equal the population's argmin and row; after
+    load() (whose control block predates the blob) it recomputes, with the same answer."""
+    N, D, p = 500, 29, "ackley"
+    mk = (lambda: ev.DE(N, D, -32.768, 32.768, seed=8)) if algo == "de" else \
+        (lambda: ev.CSO(N, D, -32.768, 32.768, block=100, seed=8))
+    a = mk()
+    for g in (0, 1, 5):
+        a.step(p, g)
+        fa, ia, ra = a.best()
+        F = a.view("F").cpu().numpy()
+        X = a.view("X").cpu().numpy()[:, :D]
+        assert fa == F.min() and ia == int(np.argmin(F)) and np.array_equal(ra, X[ia])
+    blob = a.save()
+    b = mk()
+    b.load(blob)
+    assert b.best()[:2] == a.best()[:2]
+    assert np.array_equal(b.best()[2], a.best()[2])
