@@ -9,6 +9,16 @@
 #include "evox_internal.h"
 #include "row_engine.cuh"
 
+#ifndef EVOX_CSO_U
+#define EVOX_CSO_U U        // chunks in flight per lane group (warp-row geometries)
+#endif
+#ifndef EVOX_CSO_MINB
+#define EVOX_CSO_MINB EVOX_MINB
+#endif
+#ifndef EVOX_CSO_WAVES
+#define EVOX_CSO_WAVES 1
+#endif
+
 namespace evox {
 
 namespace {
@@ -193,7 +203,7 @@ __device__ __forceinline__ CsoItem cso_item(const CsoArgs& a, long long it, uint
 // One CSO generation over this shard's whole blocks.  One work item per pair
 // (plus one for the unpaired member of an odd block), mapped like a row.
 template <int P, class G, bool UNI>
-__global__ void __launch_bounds__(256, EVOX_MINB) k_cso_gen(CsoArgs a) {
+__global__ void __launch_bounds__(256, EVOX_CSO_MINB) k_cso_gen(CsoArgs a) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
     __shared__ __align__(16) HStore<P, G> sh_h;
@@ -398,17 +408,24 @@ static long long cso_items(const CsoArgs& a) {
     return ((end + a.B - 1) / a.B - blk0) * ((a.B + 1) / 2);
 }
 
+// The CSO generation's geometry: the row geometry of ld with its own chunk count (never a
+// change of any lane's quad order, so the reduction order is the geometry's).
+#define EVOX_CSO_GEOM(G_) Geom<G_::LPR, G_::WPR, G_::WPR == 1 ? EVOX_CSO_U : G_::NU, G_::EFL>
+
 int cso_gen_grid(int problem, const CsoArgs& a, int device) {
     int g = 1;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM_ID(cso_geom_id(a.ld), {
-        g = grid_for((const void*)k_cso_gen<P_, G_, true>, row_units<G_>(cso_items(a)), device);
+        using GC_ = EVOX_CSO_GEOM(G_);
+        g = grid_for((const void*)k_cso_gen<P_, GC_, true>, row_units<GC_>(cso_items(a)), device,
+                     EVOX_CSO_WAVES);
     }));
     return g;
 }
 
 cudaError_t launch_cso_gen(int problem, const CsoArgs& a, int grid, cudaStream_t st) {
     EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM_ID(cso_geom_id(a.ld), {
-        k_cso_gen<P_, G_, U_><<<grid, 256, 0, st>>>(a);
+        using GC_ = EVOX_CSO_GEOM(G_);
+        k_cso_gen<P_, GC_, U_><<<grid, 256, 0, st>>>(a);
     })));
     return cudaGetLastError();
 }

@@ -466,6 +466,19 @@ __global__ void __launch_bounds__(256) k_pso_fin(PsoArgs a, long long t_arg) {
                    NQ);
 }
 
+#ifndef EVOX_PSO_SHORT_U
+#define EVOX_PSO_SHORT_U U  // chunks in flight of the generation kernel for short rows (<= 256)
+#endif
+// The persistent generation kernel's geometry: the row geometry of ld with its own chunk
+// count for short rows (a lane's quad order, hence every reduction order, is unchanged).
+#define EVOX_PSO_GEOM(G_) Geom<G_::LPR, G_::WPR, G_::LPR <= 8 ? EVOX_PSO_SHORT_U : G_::NU, G_::EFL>
+
+#ifndef EVOX_MID_U
+#define EVOX_MID_U 4     // chunks in flight of the cooperative kernel, warp-per-row geometry
+#endif
+#ifndef EVOX_MID_MINB
+#define EVOX_MID_MINB EVOX_MINB  // its CTAs/SM (register cap), warp-per-row geometry
+#endif
 #ifndef EVOX_MID_PF
 #define EVOX_MID_PF 1  // k_pso_run_mid: L2 prefetch of the next generation's first rows
 #endif
@@ -478,7 +491,8 @@ __global__ void __launch_bounds__(256) k_pso_fin(PsoArgs a, long long t_arg) {
 // are those of k_pso_gen (same geometry, same per-row code), so the trajectory is
 // bitwise the stepwise one.  The barrier spin is bounded (ctl->err, no hang).
 template <int P, class G, bool UNI>
-__global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB : EVOX_MINB)
+__global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB
+                                                   : (G::WPR == 1 ? EVOX_MID_MINB : EVOX_MINB))
     k_pso_run_mid(PsoArgs a, long long n) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
@@ -956,7 +970,8 @@ int pso_gen_grid(int problem, long long ld, long long rows, int device, bool wav
     }
     const int waves = geom_id(ld) == 1 && rows * ld > BIG ? 4 : 1;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
-        g = grid_for((const void*)k_pso_gen<P_, G_, true>, row_units<G_>(rows), device, waves);
+        using GP_ = EVOX_PSO_GEOM(G_);
+        g = grid_for((const void*)k_pso_gen<P_, GP_, true>, row_units<GP_>(rows), device, waves);
     }));
     return g;  // the TMA variant uses the same grid (2 CTAs/SM: 2 x 96 KB of staging)
 }
@@ -989,7 +1004,8 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
         }));
     } else {
         EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-            e = launch_pdl(k_pso_gen<P_, G_, U_>, grid, a, st);
+            using GP_ = EVOX_PSO_GEOM(G_);
+            e = launch_pdl(k_pso_gen<P_, GP_, U_>, grid, a, st);
         })));
     }
     return e != cudaSuccess ? e : cudaGetLastError();
@@ -1009,7 +1025,9 @@ cudaError_t launch_pso_run_mid(int problem, const PsoArgs& a, long long n, cudaS
     cudaGetDevice(&dev);
     cudaError_t e = cudaSuccess;
     EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-        const void* fn = (const void*)k_pso_run_mid<P_, G_, U_>;
+        using GM_ = Geom<G_::LPR, G_::WPR, G_::LPR == 32 && G_::WPR == 1 ? EVOX_MID_U : G_::NU,
+                         G_::EFL>;
+        const void* fn = (const void*)k_pso_run_mid<P_, GM_, U_>;
         const int grid = grid_for(fn, row_units<G_>(a.rows), dev);  // resident grid only
         PsoArgs aa = a;
         long long nn = n;
