@@ -507,7 +507,8 @@ struct evox_pso : Base {
     unsigned char* rec = nullptr;
     int64_t rec_stride = 0;
     int gen_grid[5] = {0, 0, 0, 0, 0};
-    bool wave = false;  // big population on the wave grid (k_pso_gen_wave + k_pso_fin)
+    bool wave[5] = {false, false, false, false, false};  // per problem: the wave grid
+                                                         // (k_pso_gen_wave + k_pso_fin)
     // in-kernel peer exchange (evox_pso_connect)
     unsigned char* mbox = nullptr;  // own mailbox (separate cudaMalloc: IPC-exportable)
     size_t mb_bytes = 0;
@@ -539,7 +540,7 @@ struct evox_pso : Base {
         a.world = world;
         a.exchange = comm != nullptr && !peer;
         a.peer = peer ? 1 : 0;
-        a.fin_kernel = (peer || wave) ? 1 : 0;
+        a.fin_kernel = peer ? 1 : 0;  // | wave[problem], set by the step
         a.mb_slot = mb_slot;
         a.peer_timeout_ns = peer_timeout_ns;
         for (int r = 0; r < evox::kMaxPeers; ++r) a.mbox[r] = peers[r];
@@ -549,8 +550,8 @@ struct evox_pso : Base {
 
 namespace {
 
-bool pso_use_wave(const evox_pso* s) {
-    return !(s->flags & EVOX_FLAG_NO_WAVE) && evox::pso_wave(s->ld, s->rows);
+bool pso_use_wave(const evox_pso* s, int problem) {
+    return !(s->flags & EVOX_FLAG_NO_WAVE) && evox::pso_wave(problem, s->ld, s->rows);
 }
 
 void pso_layout(evox_pso* s, Carver& c) {
@@ -720,9 +721,10 @@ evox_status evox_pso_init(int64_t pop, int64_t dim, const float* lb, const float
             if (e == cudaSuccess) e = cudaMemsetAsync(s->mbox, 0, s->mb_bytes, s->stream);
         }
         if (e != cudaSuccess) st = poison(s, EVOX_ERR_CUDA, "pso init", e);
-        for (int p = 0; p < 5 && st == EVOX_OK; ++p)
-            s->gen_grid[p] = evox::pso_gen_grid(p, s->ld, s->rows, s->device, pso_use_wave(s));
-        s->wave = pso_use_wave(s);
+        for (int p = 0; p < 5 && st == EVOX_OK; ++p) {
+            s->wave[p] = pso_use_wave(s, p);
+            s->gen_grid[p] = evox::pso_gen_grid(p, s->ld, s->rows, s->device, s->wave[p]);
+        }
     }
     if (st != EVOX_OK) {
         std::string keep = t_err;
@@ -757,7 +759,8 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
         if (st != EVOX_OK) return st;
     }
     if (n_gens == 0) return EVOX_OK;
-    const PsoArgs a = s->args();
+    PsoArgs a = s->args();
+    if (s->wave[problem]) a.fin_kernel = 1;  // the wave grid publishes gbest in k_pso_fin
     const int grid = s->gen_grid[problem];
     const bool no_small = (s->flags & EVOX_FLAG_NO_SMALL) != 0;  // testing: force multi-CTA
     if (!s->comm && !s->peer && !no_small && evox::pso_small(s->rows, s->ld)) {
@@ -777,7 +780,7 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
     st = run_graphed(s, (int)problem, n_gens, [&]() -> evox_status {
         CU(s, timed(s, [&] { return evox::launch_pso_gen((int)problem, a, grid, s->stream,
                                                       (s->flags & EVOX_FLAG_TMA) != 0,
-                                                      s->wave); }));
+                                                      s->wave[problem]); }));
         if (a.fin_kernel)
             CU(s, timed(s, [&] { return evox::launch_pso_fin(a, -1, s->stream); }, 0, 1));
         return pso_exchange(s);

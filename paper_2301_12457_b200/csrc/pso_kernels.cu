@@ -265,10 +265,10 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : (G::LPR == 4
 }
 
 #ifndef EVOX_WAVE_MINB
-#define EVOX_WAVE_MINB 3
+#define EVOX_WAVE_MINB 4  // CTAs/SM of the wave kernel (warp-row geometries)
 #endif
 #ifndef EVOX_WAVE_U
-#define EVOX_WAVE_U 3  // chunks in flight per lane group in the wave kernel
+#define EVOX_WAVE_U 2  // chunks in flight per lane group in the wave kernel (warp-row geometries)
 #endif
 
 // Fused PSO generation on a "wave" grid: one CTA per row block (every thread at most one
@@ -953,13 +953,18 @@ bool pso_prefetch_next(long long ld, long long rows) {
 
 #ifndef EVOX_WAVE
 // which big populations take the wave grid (bit k: geometry id k; measurement builds may
-// change it).  Measured (profiles/r02_ab_wave.txt): CTA-per-row (C5) 0.895 -> 0.923 of the
-// HBM peak; warp-per-row (H) 0.898 -> 0.891 and 4-lanes-per-row (C4) 0.770 -> 0.664: those
-// keep the persistent grid.
-#define EVOX_WAVE (1 << 2)
+// change it).  Measured same box (profiles/r02_ab_wave_h.txt): warp-per-row rows with 2 chunks
+// in flight and 4 CTAs/SM: H (Ackley) 0.894 -> 0.924, Sphere 0.913 -> 0.971, Rastrigin
+// 0.903 -> 0.939, Rosenbrock 0.898 -> 0.915 of the HBM peak; CTA-per-row (C5) 0.895 -> 0.923;
+// 4-lanes-per-row (C4) neutral -> keeps the persistent grid with its next-row prefetch.
+#define EVOX_WAVE ((1 << 1) | (1 << 2))
 #endif
-bool pso_wave(long long ld, long long rows) {
-    return rows * ld > BIG && ((EVOX_WAVE >> geom_id(ld)) & 1);
+bool pso_wave(int problem, long long ld, long long rows) {
+    const int g = geom_id(ld);
+    if (rows * ld <= BIG || !((EVOX_WAVE >> g) & 1)) return false;
+    // Griewank's warp-row kernels keep a 16 KB shared-memory column table per CTA: at 4 CTAs/SM
+    // that takes the L1 the streaming loads need (0.874 -> 0.801): persistent grid
+    return !(problem == GRIEWANK && g == 1);
 }
 
 int pso_gen_grid(int problem, long long ld, long long rows, int device, bool wave) {

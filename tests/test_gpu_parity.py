@@ -204,11 +204,13 @@ def test_pso_mid_kernel_equals_stepwise(problem, N, D):
 
 
 @pytest.mark.parametrize("problem,N,D", [("ackley", 400, 100_000), ("rosenbrock", 2000, 17_001),
-                                         ("griewank", 800, 50_000)])
+                                         ("griewank", 800, 50_000), ("ackley", 40_000, 1000),
+                                         ("rosenbrock", 34_000, 1001), ("sphere", 9_000, 3999)])
 def test_pso_wave_kernel_equals_persistent(problem, N, D):
-    """Big populations (> 2^25 elements) run the wave grid (k_pso_gen_wave: one CTA per row
-    block, 3 chunks in flight, gbest published by k_pso_fin) -- bitwise the persistent
-    grid-stride kernel (EVOX_FLAG_NO_WAVE): same per-row code and reduction order."""
+    """Big populations (> 2^25 elements) with rows of > 128 floats run the wave grid
+    (k_pso_gen_wave: one CTA per row block, fewer chunks in flight, more CTAs/SM, gbest
+    published by k_pso_fin) -- bitwise the persistent grid-stride kernel (EVOX_FLAG_NO_WAVE):
+    same per-row code and reduction order."""
     lb, ub = WL.BOUNDS[problem]
     a = ev.PSO(N, D, lb, ub, seed=17)
     a.step(problem, 4)
