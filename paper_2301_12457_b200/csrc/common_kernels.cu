@@ -14,9 +14,24 @@ namespace evox {
 
 namespace {
 
+#ifndef EVOX_EVAL_WAVES
+// waves of resident CTAs by geometry (0: one CTA per row unit).  Measured same box
+// (profiles/r02_ab_eval.txt): warp-per-row 4 waves (EH-ackley 0.916 -> 0.967, rastrigin
+// 0.906 -> 0.959, rosenbrock 0.896 -> 0.950, griewank 0.792 -> 0.857 of the HBM peak);
+// CTA-per-row one CTA per row (E5-griewank 0.782 -> 0.843); short rows unchanged (1).
+#define EVOX_EVAL_WAVES(G_) (G_::WPR > 1 ? 0 : (G_::LPR == 32 ? 4 : 1))
+#endif
+#ifndef EVOX_EVAL_MINB
+#define EVOX_EVAL_MINB 1
+#endif
+#ifndef EVOX_EVAL_U
+#define EVOX_EVAL_U U      // chunks in flight (warp-row geometries)
+#endif
+#define EVOX_EVAL_GEOM(G_) Geom<G_::LPR, G_::WPR, G_::WPR == 1 ? EVOX_EVAL_U : G_::NU, G_::EFL>
+
 // evox_eval: fit[r] = f(X[r]).
 template <int P, class G>
-__global__ void __launch_bounds__(256) k_eval(const float* __restrict__ X, long long rows,
+__global__ void __launch_bounds__(256, EVOX_EVAL_MINB) k_eval(const float* __restrict__ X, long long rows,
                                               long long D, long long ld,
                                               float* __restrict__ fit,
                                               const float* __restrict__ hg) {
@@ -146,8 +161,12 @@ cudaError_t launch_eval(int problem, const float* X, long long rows, long long D
     const float* hg = problem == GRIEWANK && geom_id(ld) == 2 ? griewank_table(ld, dev, st, no_htab)
                                                                : nullptr;
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
-        const int g = grid_for((const void*)k_eval<P_, G_>, row_units<G_>(rows), dev);
-        k_eval<P_, G_><<<g, 256, 0, st>>>(X, rows, D, ld, fit, hg);
+        using GE_ = EVOX_EVAL_GEOM(G_);
+        const int g = EVOX_EVAL_WAVES(GE_) > 0
+                          ? grid_for((const void*)k_eval<P_, GE_>, row_units<GE_>(rows), dev,
+                                     EVOX_EVAL_WAVES(GE_))
+                          : (int)row_units<GE_>(rows);
+        k_eval<P_, GE_><<<g, 256, 0, st>>>(X, rows, D, ld, fit, hg);
     }));
     return cudaGetLastError();
 }

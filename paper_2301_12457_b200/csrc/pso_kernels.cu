@@ -267,6 +267,9 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : (G::LPR == 4
 #ifndef EVOX_WAVE_MINB
 #define EVOX_WAVE_MINB 4  // CTAs/SM of the wave kernel (warp-row geometries)
 #endif
+#ifndef EVOX_ROW_U
+#define EVOX_ROW_U 3  // chunks in flight of the wave kernel, CTA-per-row geometry
+#endif
 #ifndef EVOX_WAVE_U
 #define EVOX_WAVE_U 2  // chunks in flight per lane group in the wave kernel (warp-row geometries)
 #endif
@@ -997,7 +1000,7 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
         // the wave kernel keeps fewer chunks in flight (registers for 3 CTAs/SM); the chunk
         // count never changes a lane's quad order, so the reduction order is the geometry's
         EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-            using GW_ = Geom<G_::LPR, G_::WPR, G_::WPR == 1 ? EVOX_WAVE_U : G_::NU, G_::EFL>;
+            using GW_ = Geom<G_::LPR, G_::WPR, G_::WPR == 1 ? EVOX_WAVE_U : EVOX_ROW_U, G_::EFL>;
             e = launch_pdl(k_pso_gen_wave<P_, GW_, U_>, grid, a, st);
         })));
         return e != cudaSuccess ? e : cudaGetLastError();
