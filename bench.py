@@ -44,8 +44,8 @@ def _env_int(k, d):
 def gen_kernel_name(cfg, rows, world):
     """The generation kernel evox_*_step launches for this shard (mirrors the C-ABI's
     dispatch: single-CTA persistent <= 2^14 elements, cooperative persistent <= 2^25 for
-    PSO at W = 1, the wave grid for PSO rows of > 256 floats beyond 2^25 elements (Griewank:
-    > 4096), else one
+    PSO at W = 1, beyond 2^25 elements the flat-tile kernel for PSO rows of <= 256 floats and
+    the wave grid for rows of > 256 floats (Griewank: > 4096), else one
     k_*_gen launch per generation)."""
     ld = (cfg.dim + 3) // 4 * 4
     n = rows * ld
@@ -53,8 +53,12 @@ def gen_kernel_name(cfg, rows, world):
         return f"k_pso_run_small<{cfg.problem}>"
     if cfg.algo == "pso" and world == 1 and n <= (1 << 25):
         return f"k_pso_run_mid<{cfg.problem}>"
+    if cfg.algo == "pso" and n > (1 << 25) and ld <= 256:
+        return f"k_pso_gen_flat<{cfg.problem}>"
     if cfg.algo == "pso" and n > (1 << 25) and (ld > 4096 or (ld > 256 and cfg.problem != "griewank")):
         return f"k_pso_gen_wave<{cfg.problem}>"
+    if cfg.algo == "de" and ld <= 256:
+        return f"k_de_gen_flat<{cfg.problem}>"
     return f"k_{cfg.algo}_gen<{cfg.problem}>"
 
 

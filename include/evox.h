@@ -106,8 +106,9 @@ enum {
     EVOX_FLAG_FORCE_NCCL = 1u << 3, /* world == 1: run the NCCL exchange path on a 1-rank
                                        communicator (exercises the multi-GPU code) */
     EVOX_FLAG_NO_GRAPH = 1u << 4,   /* launch generations directly, not through CUDA graphs */
-    EVOX_FLAG_NO_WAVE = 1u << 5     /* PSO, > 2^25 elements: the persistent grid-stride generation
-                                       kernel instead of the one-CTA-per-row-block wave grid */
+    EVOX_FLAG_NO_WAVE = 1u << 5     /* PSO, > 2^25 elements, and DE with rows of <= 256 floats: the
+                                       grid-stride row-walk generation kernel instead of the
+                                       one-CTA-per-row-block wave / flat-tile kernels */
 };
 
 /* Description of the last failure on the calling thread ("" if none). */

@@ -216,6 +216,147 @@ __global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_DE_SHORT_MINB : EVOX_M
 #endif
 }
 
+#ifndef EVOX_DE_FLAT_MINB
+#define EVOX_DE_FLAT_MINB 5  // CTAs/SM of k_de_gen_flat (register cap; 3/4/6: 0.818/0.816/0.857, D1)
+#endif
+#ifndef EVOX_DE_FLAT_FIN
+#define EVOX_DE_FLAT_FIN 1  // CTA minimum by relaxed atomicMin; k_de_fin publishes
+#endif
+#ifndef EVOX_DE_FLAT_PF
+#define EVOX_DE_FLAT_PF 0  // L2 prefetch: bit 0 the (local) donor rows, bit 1 the target rows
+                           // (measured: both on 0.643 vs 0.814 of the HBM peak at D1, off)
+#endif
+
+// Staged x' of one row in shared memory for the row engine (phase 2 of the flat kernels).
+struct MoverSmemDe {
+    const float4* xr;
+    float4 x[U];
+    template <bool EF>
+    __device__ __forceinline__ void load(int u, int q) { x[u] = xr[q]; }
+    template <bool EF>
+    __device__ __forceinline__ void load_late(int, int) {}
+    __device__ __forceinline__ float4 step(int u, int) { return x[u]; }
+};
+
+// DE generation for short rows (4 / 8 lanes per row geometries, ld <= 256) on a grid of one
+// CTA per G::RPC targets, in three phases (the structure of k_pso_gen_flat):
+//  0. one thread per target resolves its donors (de_indices), the buffer flags of the four
+//     rows, j_rand and f(x), and issues the L2 bulk prefetch of the target and donor rows
+//     (400 B each at D1): the scattered-row DRAM stream starts at once, not behind registers;
+//  1. flat: the tile's RPC x NQ trial quads, thread i: quads i, i + 256, ... -- each trial quad
+//     is exactly MoverDe::step's (same Philox counter (q, global row, t, 10), op order, clip,
+//     zero padding), written to the other buffer and staged in shared memory;
+//  2. the geometry's row engine folds f(u) from the staged rows in the geometry's order
+//     (bitwise k_de_gen's), then the greedy "<=" replacement and the grid argmin.
+template <int P, class G, bool UNI>
+__global__ void __launch_bounds__(256, EVOX_DE_FLAT_MINB) k_de_gen_flat(DeArgs a) {
+    static_assert(G::WPR == 1, "flat phase: warp-row geometries only");
+    extern __shared__ __align__(128) unsigned char de_flat_smem[];
+    float4* xs = reinterpret_cast<float4*>(de_flat_smem);  // [RPC][NQ] (+ [ld] htab)
+    __shared__ Fit<P> sh_acc[1];
+    __shared__ float sh_head[1];
+    __shared__ const float4* sh_src[G::RPC][4];  // target, donors r1, r2, r3
+    __shared__ int sh_jr[G::RPC];
+    __shared__ float sh_fx[G::RPC];
+    __shared__ unsigned char sh_si[G::RPC];
+    const int NQ = (int)(a.ld >> 2);
+    const float* htab = HTable<P, G>::fill(reinterpret_cast<float*>(xs + G::RPC * NQ), a.ld);
+    const RowMap<G> m(NQ);
+    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
+    const int p = (int)(t & 1);
+    const long long row0 = (long long)blockIdx.x * G::RPC;
+    const int nrow = a.rows - row0 < G::RPC ? (int)(a.rows - row0) : G::RPC;
+    // phase 0: per-target resolution + prefetch
+    if ((int)threadIdx.x < nrow) {
+        const long long rw = row0 + threadIdx.x;
+        long long r[3];
+        de_indices(a, a.row0 + rw, (uint32_t)t, r);
+        const int si = a.sel[p][rw];
+        const float4* src[4];
+        src[0] = reinterpret_cast<const float4*>(a.buf[si] + rw * a.ld);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int w = de_owner(a, r[k]);
+            const long long lr = r[k] - a.prow0[w];
+            const int fl = a.psel[w][p][lr];
+            src[k + 1] = reinterpret_cast<const float4*>(a.pbuf[w][fl] + lr * a.ld);
+#if EVOX_DE_FLAT_PF & 1
+            if (w == a.rank) prefetch_l2(src[k + 1], a.ld * 4);
+#endif
+        }
+#if EVOX_DE_FLAT_PF & 2
+        prefetch_l2(src[0], a.ld * 4);
+#endif
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sh_src[threadIdx.x][k] = src[k];
+        const uint4 jw = Philox::run(make_uint4(0u, (uint32_t)(a.row0 + rw), (uint32_t)t, 9u), a.rk);
+        sh_jr[threadIdx.x] = (int)(((unsigned long long)jw.x * (unsigned long long)a.D) >> 32);
+        sh_fx[threadIdx.x] = a.f[p][rw];
+        sh_si[threadIdx.x] = (unsigned char)si;
+    }
+    __syncthreads();
+    // phase 1: flat walk of the tile's trial quads (r = i / NQ exactly: i < 2^11, NQ <= 64)
+    const int n = nrow * NQ;
+    const uint32_t magic = (1u << 20) / (uint32_t)NQ + 1u;
+    for (int i = threadIdx.x; i < n; i += 256) {
+        const int r = (int)(((uint32_t)i * magic) >> 20);
+        const int q = i - r * NQ;
+        MoverDe<UNI> mv(a);
+        mv.Xi = sh_src[r][0];
+        mv.Xa = sh_src[r][1];
+        mv.Xb = sh_src[r][2];
+        mv.Xc = sh_src[r][3];
+        mv.Out = reinterpret_cast<float4*>(a.buf[sh_si[r] ^ 1] + (row0 + r) * a.ld);
+        mv.jrand = sh_jr[r];
+        mv.row_g = (uint32_t)(a.row0 + row0 + r);
+        mv.t = (uint32_t)t;
+        mv.template load<G::EFL>(0, q);
+        xs[i] = mv.step(0, q);
+    }
+    __syncthreads();
+    // phase 2: f(u) in the geometry's order, greedy replacement, argmin key
+    unsigned long long best = ~0ull;
+    {
+        const long long row = m.first;
+        const bool ok = row < a.rows;
+        MoverSmemDe ms;
+        ms.xr = xs + (ok ? row - row0 : 0) * NQ;
+        Fit<P> acc;
+        float hx, tx;
+        bool tv;
+        NoPrefetch pf;
+        walk_segment<P, G>(ms, 0, NQ, a.D, ok, acc, hx, tx, tv, pf, htab);
+        const float fu = reduce_row<P, G>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
+        if (m.leader && ok) {
+            const int lr = (int)(row - row0);
+            const float fx = sh_fx[lr];
+            const int si = sh_si[lr];
+            const bool accept = nan_inf(fu) <= nan_inf(fx);  // S:325, NaN as +inf
+            const float fn = accept ? fu : fx;
+            a.sel[p ^ 1][row] = (unsigned char)(accept ? (si ^ 1) : si);
+            a.f[p ^ 1][row] = fn;
+            best = make_key(fn, a.row0 + row);
+        }
+    }
+#if EVOX_DE_FLAT_FIN
+    // the CTA's minimum key: one relaxed atomicMin, no fence / ticket (k_de_fin publishes
+    // after the kernel boundary)
+    __shared__ unsigned long long sh_k[WARPS];
+    best = warp_min_u64(best);
+    if (lane_id() == 0) sh_k[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long k = sh_k[0];
+#pragma unroll
+        for (int i = 1; i < WARPS; ++i) k = sh_k[i] < k ? sh_k[i] : k;
+        if (k != ~0ull) atomicMin(&a.ctl->gen_key, k);
+    }
+#else
+    unsigned long long key;
+    if (grid_argmin(a.ctl, best, &key, a.peer != 0)) de_finalize(a, key, t + 1);
+#endif
+}
+
 // End of a DE generation launched without the in-kernel grid argmin (EVOX_DE_FIN): the
 // generation's minimum, hist, and (peers) the end-of-generation barrier + global minimum.
 // The kernel boundary orders every row the generation wrote before the peer publication.
@@ -318,8 +459,15 @@ cudaError_t launch_de_tell0(const DeArgs& a, cudaStream_t st) {
 // rows (never a change of any lane's quad order, so the reduction order is the geometry's).
 #define EVOX_DE_GEOM(G_) Geom<G_::LPR, G_::WPR, G_::LPR == 4 ? EVOX_DE_U : G_::NU, G_::EFL>
 
-int de_gen_grid(int problem, long long ld, long long rows, int device) {
+// Short rows (4 / 8 lanes per row) take the flat-tile kernel unless `no_flat`.
+static bool de_flat(long long ld, bool no_flat) { return !no_flat && geom_id(ld) != 1 && geom_id(ld) != 2; }
+
+int de_gen_grid(int problem, long long ld, long long rows, int device, bool no_flat) {
     int g = 1;
+    if (de_flat(ld, no_flat)) {
+        EVOX_DISPATCH_GEOM(ld, { g = (int)row_units<G_>(rows); });
+        return g;
+    }
     EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(ld, {
         using GD_ = EVOX_DE_GEOM(G_);
         g = grid_for((const void*)k_de_gen<P_, GD_, true>, row_units<GD_>(rows), device,
@@ -328,7 +476,18 @@ int de_gen_grid(int problem, long long ld, long long rows, int device) {
     return g;
 }
 
-cudaError_t launch_de_gen(int problem, const DeArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_de_gen(int problem, const DeArgs& a, int grid, cudaStream_t st, bool no_flat) {
+    if (de_flat(a.ld, no_flat)) {
+        EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
+            if constexpr (G_::WPR == 1 && G_::LPR <= 8) {
+                const size_t smem = (size_t)G_::RPC * (size_t)a.ld * 4 +
+                                    (problem == GRIEWANK ? (size_t)a.ld * 4 : 0);
+                k_de_gen_flat<P_, G_, U_><<<grid, 256, smem, st>>>(a);
+            }
+        })));
+        if (EVOX_DE_FLAT_FIN) k_de_fin<<<1, 32, 0, st>>>(a);
+        return cudaGetLastError();
+    }
     EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
         using GD_ = EVOX_DE_GEOM(G_);
         k_de_gen<P_, GD_, U_><<<grid, 256, 0, st>>>(a);

@@ -1818,7 +1818,8 @@ evox_status evox_de_init(int64_t pop, int64_t dim, const float* lb, const float*
             e = cudaMemsetAsync(s->mbox, 0, (size_t)32 * (s->world > 1 ? s->world : 1), s->stream);
         if (e != cudaSuccess) st = poison(s, EVOX_ERR_CUDA, "de init", e);
         for (int p = 0; p < 5 && st == EVOX_OK; ++p)
-            s->gen_grid[p] = evox::de_gen_grid(p, s->ld, s->rows, s->device);
+            s->gen_grid[p] = evox::de_gen_grid(p, s->ld, s->rows, s->device,
+                                               (s->flags & EVOX_FLAG_NO_WAVE) != 0);
     }
     if (st != EVOX_OK) {
         std::string keep = t_err;
@@ -1856,7 +1857,8 @@ evox_status evox_de_step(evox_de* s, evox_problem problem, int64_t n_gens) {
     if (n_gens == 0) return EVOX_OK;
     const int grid = s->gen_grid[problem];
     st = run_graphed(s, (int)problem, n_gens, [&]() -> evox_status {
-        CU(s, timed(s, [&] { return evox::launch_de_gen((int)problem, a, grid, s->stream); }));
+        CU(s, timed(s, [&] { return evox::launch_de_gen((int)problem, a, grid, s->stream,
+                                                             (s->flags & EVOX_FLAG_NO_WAVE) != 0); }));
         return EVOX_OK;
     });
     if (st != EVOX_OK) return st;

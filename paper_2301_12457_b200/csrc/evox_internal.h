@@ -170,8 +170,9 @@ cudaError_t launch_argmin_rows(const float* f, long long rows, long long row0,
 
 cudaError_t launch_de_init(const DeArgs& a, cudaStream_t st);
 cudaError_t launch_de_tell0(const DeArgs& a, cudaStream_t st);
-int de_gen_grid(int problem, long long ld, long long rows, int device);
-cudaError_t launch_de_gen(int problem, const DeArgs& a, int grid, cudaStream_t st);
+// no_flat: the row-walk kernel even for short rows (EVOX_FLAG_NO_WAVE; tests)
+int de_gen_grid(int problem, long long ld, long long rows, int device, bool no_flat);
+cudaError_t launch_de_gen(int problem, const DeArgs& a, int grid, cudaStream_t st, bool no_flat);
 cudaError_t launch_de_materialize(const DeArgs& a, cudaStream_t st);
 cudaError_t launch_de_gather(const DeArgs& a, float* dst, cudaStream_t st);
 

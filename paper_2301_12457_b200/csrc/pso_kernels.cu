@@ -329,6 +329,172 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : EVOX_WAVE_MI
     }
 }
 
+#ifndef EVOX_FLAT_K
+#define EVOX_FLAT_K 1  // quads per thread per batch of the flat phase (with the tile's L2 prefetch)
+#endif
+#ifndef EVOX_FLAT_MINB
+#define EVOX_FLAT_MINB 4  // its CTAs/SM (register cap)
+#endif
+#ifndef EVOX_FLAT_EF
+#define EVOX_FLAT_EF 1  // evict-first loads in the flat phase
+#endif
+#ifndef EVOX_FLAT_PF
+#define EVOX_FLAT_PF 3  // bulk L2 prefetch of the CTA's tile at its start: bit 0 X, V; bit 1 P rows
+#endif
+#ifndef EVOX_FLAT_PF_GRIEWANK
+#define EVOX_FLAT_PF_GRIEWANK 1
+#endif
+#ifndef EVOX_FLAT_MINB_GRIEWANK
+#define EVOX_FLAT_MINB_GRIEWANK 6
+#endif
+
+// The staged x' of one row in shared memory, walked by the row engine (phase 2 of
+// k_pso_gen_flat): the geometry's own loads, chunk order and fitness fold, so the fitness
+// is bitwise the one the moving lanes would have folded from registers.
+struct MoverSmem {
+    const float4* xr;
+    float4 x[U];
+    template <bool EF>
+    __device__ __forceinline__ void load(int u, int q) { x[u] = xr[q]; }
+    template <bool EF>
+    __device__ __forceinline__ void load_late(int, int) {}
+    __device__ __forceinline__ float4 step(int u, int) { return x[u]; }
+};
+
+// Fused PSO generation for short rows (4 / 8 lanes per row geometries, ld <= 256) on a wave
+// grid of one CTA per G::RPC rows, in two phases:
+//  1. flat: the CTA's RPC x NQ quads are contiguous in X, V, P, so its threads walk them as one
+//     flat range (thread i: quads i, i + 256, ...; EVOX_FLAT_K in flight) -- every warp
+//     instruction reads 512 contiguous bytes instead of 4-8 separate 64-byte row pieces, and
+//     no lane idles on a row's ragged end.  Each quad is moved by exactly MoverPso::step (same
+//     Philox counters (q, global row, t, tag), op order, clip, zero padding, lazy pbest) and its
+//     x' is staged in shared memory;
+//  2. the geometry's row engine (walk_segment / reduce_row over RowMap<G>, reading the staged
+//     x') folds the fitness in the geometry's order: bitwise the f of k_pso_gen (R-11), then
+//     the per-row tell and the CTA's argmin key (one relaxed atomicMin; gbest is published by
+//     k_pso_fin, as for k_pso_gen_wave).
+// The CTA's first act is a bulk L2 prefetch of its whole tile (X, V; P of the rows whose pbest
+// copy is not pending), so the DRAM stream never waits on registers, nor on phase 2.
+// Micro of this access pattern (scripts/micro/short.cu, profiles/r02_micro_short.txt):
+// 6.84 TB/s with Philox against 5.86 for the 4-lanes-per-row persistent walk.  Measured
+// (profiles/r02_ab_flat.txt, same box): C4g 0.767 -> 0.842, C4r 0.781 -> 0.911 of the HBM
+// peak with the prefetch (0.81 / 0.79 without it; 2 quads per batch / 3 CTAs/SM lose).
+// Griewank (the heaviest fitness fold, phase 2) measured best with more CTAs/SM and only the
+// contiguous X/V tile prefetched: C4g 0.842 -> 0.874 (C4r loses 5 points with the same).
+template <int P>
+__host__ __device__ constexpr int flat_minb() { return P == GRIEWANK ? EVOX_FLAT_MINB_GRIEWANK : EVOX_FLAT_MINB; }
+template <int P>
+__host__ __device__ constexpr int flat_pf() { return P == GRIEWANK ? EVOX_FLAT_PF_GRIEWANK : EVOX_FLAT_PF; }
+
+template <int P, class G, bool UNI>
+__global__ void __launch_bounds__(256, flat_minb<P>()) k_pso_gen_flat(PsoArgs a) {
+    static_assert(G::WPR == 1, "flat phase: warp-row geometries only");
+    extern __shared__ __align__(128) unsigned char flat_smem_buf[];
+    float4* xs = reinterpret_cast<float4*>(flat_smem_buf);  // [RPC][NQ] staged x' (+ [ld] htab)
+    __shared__ Fit<P> sh_acc[1];
+    __shared__ float sh_head[1];
+    __shared__ unsigned char sh_pend[G::RPC];
+    __shared__ unsigned long long sh_k[WARPS];
+    const int NQ = (int)(a.ld >> 2);
+    const float* htab = HTable<P, G>::fill(reinterpret_cast<float*>(xs + G::RPC * NQ), a.ld);
+    const RowMap<G> m(NQ);
+    const long long row0 = (long long)blockIdx.x * G::RPC;
+    const int nrow = a.rows - row0 < G::RPC ? (int)(a.rows - row0) : G::RPC;
+    pdl_wait();               // the previous generation (G, imp, pf, t) is complete
+    pdl_launch_dependents();
+    const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
+    const int n = nrow * NQ;
+    const float4* Xt = reinterpret_cast<const float4*>(a.X) + row0 * NQ;
+    const float4* Vt = reinterpret_cast<const float4*>(a.V) + row0 * NQ;
+    const float4* Pt = reinterpret_cast<const float4*>(a.P) + row0 * NQ;
+    if (threadIdx.x < nrow) {
+        const unsigned char pd = a.imp[row0 + threadIdx.x];
+        sh_pend[threadIdx.x] = pd;
+#if EVOX_FLAT_PF
+        // the whole tile HBM -> L2 at once (X, V contiguous; P per row unless its pbest copy
+        // is pending): the DRAM stream runs ahead of the register loads, phase 2 included
+        if ((flat_pf<P>() & 1) && threadIdx.x == 0) {
+            prefetch_l2(Xt, (long long)n * 16);
+            prefetch_l2(Vt, (long long)n * 16);
+        }
+        if ((flat_pf<P>() & 2) && !pd) prefetch_l2(Pt + threadIdx.x * NQ, (long long)NQ * 16);
+#endif
+    }
+    const long long row = m.first;
+    const bool ok = row < a.rows;
+    float pf_old = 0.0f;
+    if (m.leader && ok) pf_old = a.pf[row];
+    __syncthreads();
+    // phase 1: flat walk of the tile (r = i / NQ exactly: i < 2^11, NQ <= 64)
+    const uint32_t magic = (1u << 20) / (uint32_t)NQ + 1u;
+    constexpr int K = EVOX_FLAT_K;
+    for (int b = 0; b < n; b += 256 * K) {
+        float4 x[K], v[K], p[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int i = b + 256 * k + (int)threadIdx.x;
+            if (i < n) {
+                x[k] = ld_stream<EVOX_FLAT_EF != 0>(Xt + i);
+                v[k] = ld_stream<EVOX_FLAT_EF != 0>(Vt + i);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int i = b + 256 * k + (int)threadIdx.x;
+            if (i < n) {
+                const int r = (int)(((uint32_t)i * magic) >> 20);
+                if (!sh_pend[r]) p[k] = ld_stream<EVOX_FLAT_EF != 0>(Pt + i);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int i = b + 256 * k + (int)threadIdx.x;
+            if (i < n) {
+                const int r = (int)(((uint32_t)i * magic) >> 20);
+                const int q = i - r * NQ;
+                MoverPso<UNI, false> mv(a, row0 + r, (uint32_t)t, sh_pend[r] != 0);
+                mv.x[0] = x[k];
+                mv.v[0] = v[k];
+                mv.p[0] = p[k];
+                xs[i] = mv.step(0, q);
+            }
+        }
+    }
+    __syncthreads();
+    // phase 2: the geometry's fitness fold over the staged rows, tell, argmin key
+    unsigned long long best = ~0ull;
+    {
+        MoverSmem ms;
+        ms.xr = xs + (ok ? row - row0 : 0) * NQ;
+        Fit<P> acc;
+        float hx, tx;
+        bool tv;
+        NoPrefetch pf;
+        walk_segment<P, G>(ms, 0, NQ, a.D, ok, acc, hx, tx, tv, pf, htab);
+        const float f = reduce_row<P, G>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
+        if (m.leader && ok) {
+            const bool imp = f < pf_old;  // per-row tell (A11): strict, NaN never improves
+            a.f[row] = f;
+            a.imp[row] = imp ? 1 : 0;
+            if (imp) a.pf[row] = f;
+            best = make_key(f, a.row0 + row);
+        }
+    }
+    best = warp_min_u64(best);
+    if (lane_id() == 0) sh_k[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long k = sh_k[0];
+#pragma unroll
+        for (int i = 1; i < WARPS; ++i) k = sh_k[i] < k ? sh_k[i] : k;
+        if (k != ~0ull) atomicMin(&a.ctl->gen_key, k);
+    }
+}
+
+inline size_t flat_smem(int problem, long long ld, int rpc) {
+    return (size_t)rpc * (size_t)ld * 4 + (problem == GRIEWANK ? (size_t)ld * 4 : 0);
+}
+
 // Copy `n` quads src -> dst with this grid's threads, 4 float4 loads in flight per thread.
 __device__ __forceinline__ void grid_copy4(float4* dst, const float4* src, long long n) {
     const long long nth = (long long)gridDim.x * blockDim.x;
@@ -959,12 +1125,14 @@ bool pso_prefetch_next(long long ld, long long rows) {
 // change it).  Measured same box (profiles/r02_ab_wave_h.txt): warp-per-row rows with 2 chunks
 // in flight and 4 CTAs/SM: H (Ackley) 0.894 -> 0.924, Sphere 0.913 -> 0.971, Rastrigin
 // 0.903 -> 0.939, Rosenbrock 0.898 -> 0.915 of the HBM peak; CTA-per-row (C5) 0.895 -> 0.923;
-// 4-lanes-per-row (C4) neutral -> keeps the persistent grid with its next-row prefetch.
-#define EVOX_WAVE ((1 << 1) | (1 << 2))
+// short rows (4 / 8 lanes per row) run k_pso_gen_flat on the same grid (C4g 0.767 -> 0.842,
+// C4r 0.781 -> 0.911).
+#define EVOX_WAVE ((1 << 0) | (1 << 1) | (1 << 2) | (1 << 3))
 #endif
 bool pso_wave(int problem, long long ld, long long rows) {
     const int g = geom_id(ld);
     if (rows * ld <= BIG || !((EVOX_WAVE >> g) & 1)) return false;
+    if (g == 0 || g == 3) return true;  // short rows: k_pso_gen_flat
     // Griewank's warp-row kernels keep a 16 KB shared-memory column table per CTA: at 4 CTAs/SM
     // that takes the L1 the streaming loads need (0.874 -> 0.801): persistent grid
     return !(problem == GRIEWANK && g == 1);
@@ -1000,8 +1168,14 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
         // the wave kernel keeps fewer chunks in flight (registers for 3 CTAs/SM); the chunk
         // count never changes a lane's quad order, so the reduction order is the geometry's
         EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-            using GW_ = Geom<G_::LPR, G_::WPR, G_::WPR == 1 ? EVOX_WAVE_U : EVOX_ROW_U, G_::EFL>;
-            e = launch_pdl(k_pso_gen_wave<P_, GW_, U_>, grid, a, st);
+            if constexpr (G_::WPR == 1 && G_::LPR <= 8) {
+                // short rows: flat tile walk + the geometry's fitness fold (bitwise k_pso_gen)
+                e = launch_pdl(k_pso_gen_flat<P_, G_, U_>, grid, a, st,
+                               flat_smem(problem, a.ld, G_::RPC));
+            } else {
+                using GW_ = Geom<G_::LPR, G_::WPR, G_::WPR == 1 ? EVOX_WAVE_U : EVOX_ROW_U, G_::EFL>;
+                e = launch_pdl(k_pso_gen_wave<P_, GW_, U_>, grid, a, st);
+            }
         })));
         return e != cudaSuccess ? e : cudaGetLastError();
     }

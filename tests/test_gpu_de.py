@@ -96,6 +96,25 @@ def test_de_graphed_equals_stepwise_and_view_neutral():
     assert fa == a.view("F").cpu().numpy().min() and np.array_equal(ra, _state(a, D)[0][ia])
 
 
+@pytest.mark.parametrize("problem,N,D", [("sphere", 3000, 100), ("rosenbrock", 1001, 97),
+                                         ("griewank", 777, 250), ("ackley", 5000, 16),
+                                         ("rastrigin", 70, 128), ("rosenbrock", 200, 5)])
+def test_de_flat_kernel_equals_row_walk(problem, N, D):
+    """Rows of <= 256 floats run the flat-tile DE kernel (k_de_gen_flat: donors resolved and
+    L2-prefetched per target, the tile's trial quads walked flat, f(u) folded from shared
+    memory in the geometry's order) -- bitwise the row-walk kernel (EVOX_FLAG_NO_WAVE)."""
+    lb, ub = WL.BOUNDS[problem]
+    a = ev.DE(N, D, lb, ub, seed=23)
+    a.step(problem, 12)
+    b = ev.DE(N, D, lb, ub, seed=23, flags=E.FLAG_NO_WAVE)
+    b.step(problem, 12)
+    xa, fa = _state(a, D)
+    xb, fb = _state(b, D)
+    assert np.array_equal(xa, xb) and np.array_equal(fa, fb)
+    assert np.array_equal(a.history(), b.history())
+    assert a.best()[:2] == b.best()[:2]
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("gens", [1, 2, 7])
 def test_de_best_row_before_any_gather(gens):

@@ -205,7 +205,11 @@ def test_pso_mid_kernel_equals_stepwise(problem, N, D):
 
 @pytest.mark.parametrize("problem,N,D", [("ackley", 400, 100_000), ("rosenbrock", 2000, 17_001),
                                          ("griewank", 800, 50_000), ("ackley", 40_000, 1000),
-                                         ("rosenbrock", 34_000, 1001), ("sphere", 9_000, 3999)])
+                                         ("rosenbrock", 34_000, 1001), ("sphere", 9_000, 3999),
+                                         # short rows: k_pso_gen_flat (4 / 8 lanes per row)
+                                         ("griewank", 340_001, 100), ("rosenbrock", 340_003, 97),
+                                         ("ackley", 140_000, 250), ("sphere", 600_000, 60),
+                                         ("rastrigin", 2_100_003, 16), ("rosenbrock", 400_001, 128)])
 def test_pso_wave_kernel_equals_persistent(problem, N, D):
     """Big populations (> 2^25 elements) with rows of > 128 floats run the wave grid
     (k_pso_gen_wave: one CTA per row block, fewer chunks in flight, more CTAs/SM, gbest
