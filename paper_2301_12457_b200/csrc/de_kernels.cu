@@ -227,17 +227,6 @@ __global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_DE_SHORT_MINB : EVOX_M
                            // (measured: both on 0.643 vs 0.814 of the HBM peak at D1, off)
 #endif
 
-// Staged x' of one row in shared memory for the row engine (phase 2 of the flat kernels).
-struct MoverSmemDe {
-    const float4* xr;
-    float4 x[U];
-    template <bool EF>
-    __device__ __forceinline__ void load(int u, int q) { x[u] = xr[q]; }
-    template <bool EF>
-    __device__ __forceinline__ void load_late(int, int) {}
-    __device__ __forceinline__ float4 step(int u, int) { return x[u]; }
-};
-
 // DE generation for short rows (4 / 8 lanes per row geometries, ld <= 256) on a grid of one
 // CTA per G::RPC targets, in three phases (the structure of k_pso_gen_flat):
 //  0. one thread per target resolves its donors (de_indices), the buffer flags of the four
@@ -252,7 +241,7 @@ template <int P, class G, bool UNI>
 __global__ void __launch_bounds__(256, EVOX_DE_FLAT_MINB) k_de_gen_flat(DeArgs a) {
     static_assert(G::WPR == 1, "flat phase: warp-row geometries only");
     extern __shared__ __align__(128) unsigned char de_flat_smem[];
-    float4* xs = reinterpret_cast<float4*>(de_flat_smem);  // [RPC][NQ] (+ [ld] htab)
+    float4* st = reinterpret_cast<float4*>(de_flat_smem);  // staged tile (+ [ld] htab)
     __shared__ Fit<P> sh_acc[1];
     __shared__ float sh_head[1];
     __shared__ const float4* sh_src[G::RPC][4];  // target, donors r1, r2, r3
@@ -260,7 +249,9 @@ __global__ void __launch_bounds__(256, EVOX_DE_FLAT_MINB) k_de_gen_flat(DeArgs a
     __shared__ float sh_fx[G::RPC];
     __shared__ unsigned char sh_si[G::RPC];
     const int NQ = (int)(a.ld >> 2);
-    const float* htab = HTable<P, G>::fill(reinterpret_cast<float*>(xs + G::RPC * NQ), a.ld);
+    const int tq = G::RPC * NQ;  // staged quads per component
+    const float* htab =
+        HTable<P, G>::fill(reinterpret_cast<float*>(st + tq * stage_comps<P>()), a.ld);
     const RowMap<G> m(NQ);
     const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
     const int p = (int)(t & 1);
@@ -311,7 +302,7 @@ __global__ void __launch_bounds__(256, EVOX_DE_FLAT_MINB) k_de_gen_flat(DeArgs a
         mv.row_g = (uint32_t)(a.row0 + row0 + r);
         mv.t = (uint32_t)t;
         mv.template load<G::EFL>(0, q);
-        xs[i] = mv.step(0, q);
+        stage_quad<P>(st, tq, i, q, mv.step(0, q), htab);
     }
     __syncthreads();
     // phase 2: f(u) in the geometry's order, greedy replacement, argmin key
@@ -319,14 +310,8 @@ __global__ void __launch_bounds__(256, EVOX_DE_FLAT_MINB) k_de_gen_flat(DeArgs a
     {
         const long long row = m.first;
         const bool ok = row < a.rows;
-        MoverSmemDe ms;
-        ms.xr = xs + (ok ? row - row0 : 0) * NQ;
-        Fit<P> acc;
-        float hx, tx;
-        bool tv;
-        NoPrefetch pf;
-        walk_segment<P, G>(ms, 0, NQ, a.D, ok, acc, hx, tx, tv, pf, htab);
-        const float fu = reduce_row<P, G>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
+        const float fu = fold_staged_row<P, G>(st, tq, ok ? (int)(row - row0) : 0, NQ, a.D, ok,
+                                               htab, sh_acc, sh_head);
         if (m.leader && ok) {
             const int lr = (int)(row - row0);
             const float fx = sh_fx[lr];
@@ -480,8 +465,10 @@ cudaError_t launch_de_gen(int problem, const DeArgs& a, int grid, cudaStream_t s
     if (de_flat(a.ld, no_flat)) {
         EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
             if constexpr (G_::WPR == 1 && G_::LPR <= 8) {
-                const size_t smem = (size_t)G_::RPC * (size_t)a.ld * 4 +
-                                    (problem == GRIEWANK ? (size_t)a.ld * 4 : 0);
+                const size_t smem = flat_stage_bytes<P_>(G_::RPC, a.ld);
+                if (smem > 48 * 1024)
+                    cudaFuncSetAttribute(k_de_gen_flat<P_, G_, U_>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 k_de_gen_flat<P_, G_, U_><<<grid, 256, smem, st>>>(a);
             }
         })));

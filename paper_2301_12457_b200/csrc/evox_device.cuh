@@ -272,4 +272,86 @@ __device__ __forceinline__ void fit_quad<ROSENBROCK>(Fit<ROSENBROCK>& acc, float
     if (j0 + 3 < D) acc.pair(x.z, x.w);
 }
 
+// ---- split fitness fold (the flat-tile kernels): fit_quad == fold_quad(pre_quad(x)).
+// pre_quad computes every per-element quantity that does not depend on the running
+// accumulator (the expensive part: sin^2 terms, products) where all lanes of a CTA take part;
+// fold_quad then applies exactly fit_quad's accumulator operations, in the same order, to the
+// staged values -- so a lane that folds a row from staged pre-terms produces bitwise the value
+// it would have folded from x.  One float4 per quad (A) or two (A, B: PRE_COMPS == 2).
+// Rosenbrock is not split (its pairs straddle quads; the row engine folds it from x).
+template <int P>
+__host__ __device__ constexpr int pre_comps() { return (P == ACKLEY || P == GRIEWANK) ? 2 : 1; }
+
+template <int P>
+__device__ __forceinline__ void pre_quad(float4 x, int j0, const float* htab, float4& A, float4& B);
+template <>
+__device__ __forceinline__ void pre_quad<SPHERE>(float4 x, int, const float*, float4& A, float4&) {
+    A = x;  // s = fmaf(x, x, s)
+}
+template <>
+__device__ __forceinline__ void pre_quad<ACKLEY>(float4 x, int, const float*, float4& A, float4& B) {
+    A = x;  // s2 = fmaf(x, x, s2); ss = fmaf(sn, sn, ss)
+    B = make_float4(sinpi_red(x.x), sinpi_red(x.y), sinpi_red(x.z), sinpi_red(x.w));
+}
+__device__ __forceinline__ float rastrigin_term(float x) {
+    const float sn = sinpi_red(x);
+    return __fmaf_rn(__fmul_rn(20.0f, sn), sn, __fmul_rn(x, x));
+}
+template <>
+__device__ __forceinline__ void pre_quad<RASTRIGIN>(float4 x, int, const float*, float4& A,
+                                                    float4&) {
+    A = make_float4(rastrigin_term(x.x), rastrigin_term(x.y), rastrigin_term(x.z),
+                    rastrigin_term(x.w));  // s = s + term
+}
+__device__ __forceinline__ float griewank_a(float x, float h) {
+    const float sn = sinpi_red(__fmul_rn(x, h));
+    return __fmul_rn(2.0f, __fmul_rn(sn, sn));
+}
+template <>
+__device__ __forceinline__ void pre_quad<GRIEWANK>(float4 x, int j0, const float* htab, float4& A,
+                                                   float4& B) {
+    float4 h;
+    if (htab) {
+        h = *reinterpret_cast<const float4*>(htab + j0);
+    } else {
+        h = make_float4(griewank_h(j0), griewank_h(j0 + 1), griewank_h(j0 + 2),
+                        griewank_h(j0 + 3));
+    }
+    A = x;  // s2 = fmaf(x, x, s2); q = fmaf(-q, a, q + a)
+    B = make_float4(griewank_a(x.x, h.x), griewank_a(x.y, h.y), griewank_a(x.z, h.z),
+                    griewank_a(x.w, h.w));
+}
+
+template <int P>
+__device__ __forceinline__ void fold_elem(Fit<P>& acc, float a, float b);
+template <>
+__device__ __forceinline__ void fold_elem<SPHERE>(Fit<SPHERE>& acc, float a, float) {
+    acc.s = __fmaf_rn(a, a, acc.s);
+}
+template <>
+__device__ __forceinline__ void fold_elem<ACKLEY>(Fit<ACKLEY>& acc, float a, float b) {
+    acc.s2 = __fmaf_rn(a, a, acc.s2);
+    acc.ss = __fmaf_rn(b, b, acc.ss);
+}
+template <>
+__device__ __forceinline__ void fold_elem<RASTRIGIN>(Fit<RASTRIGIN>& acc, float a, float) {
+    acc.s = __fadd_rn(acc.s, a);
+}
+template <>
+__device__ __forceinline__ void fold_elem<GRIEWANK>(Fit<GRIEWANK>& acc, float a, float b) {
+    acc.s2 = __fmaf_rn(a, a, acc.s2);
+    acc.q = __fmaf_rn(-acc.q, b, __fadd_rn(acc.q, b));
+}
+template <int P>
+__device__ __forceinline__ void fold_quad(Fit<P>& acc, float4 A, float4 B, int j0, int D) {
+    if (j0 + 3 < D) {
+        fold_elem<P>(acc, A.x, B.x); fold_elem<P>(acc, A.y, B.y);
+        fold_elem<P>(acc, A.z, B.z); fold_elem<P>(acc, A.w, B.w);
+    } else {
+        if (j0 < D) fold_elem<P>(acc, A.x, B.x);
+        if (j0 + 1 < D) fold_elem<P>(acc, A.y, B.y);
+        if (j0 + 2 < D) fold_elem<P>(acc, A.z, B.z);
+    }
+}
+
 }  // namespace evox

@@ -342,24 +342,11 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : EVOX_WAVE_MI
 #define EVOX_FLAT_PF 3  // bulk L2 prefetch of the CTA's tile at its start: bit 0 X, V; bit 1 P rows
 #endif
 #ifndef EVOX_FLAT_PF_GRIEWANK
-#define EVOX_FLAT_PF_GRIEWANK 1
+#define EVOX_FLAT_PF_GRIEWANK EVOX_FLAT_PF
 #endif
 #ifndef EVOX_FLAT_MINB_GRIEWANK
-#define EVOX_FLAT_MINB_GRIEWANK 6
+#define EVOX_FLAT_MINB_GRIEWANK EVOX_FLAT_MINB
 #endif
-
-// The staged x' of one row in shared memory, walked by the row engine (phase 2 of
-// k_pso_gen_flat): the geometry's own loads, chunk order and fitness fold, so the fitness
-// is bitwise the one the moving lanes would have folded from registers.
-struct MoverSmem {
-    const float4* xr;
-    float4 x[U];
-    template <bool EF>
-    __device__ __forceinline__ void load(int u, int q) { x[u] = xr[q]; }
-    template <bool EF>
-    __device__ __forceinline__ void load_late(int, int) {}
-    __device__ __forceinline__ float4 step(int u, int) { return x[u]; }
-};
 
 // Fused PSO generation for short rows (4 / 8 lanes per row geometries, ld <= 256) on a wave
 // grid of one CTA per G::RPC rows, in two phases:
@@ -379,8 +366,9 @@ struct MoverSmem {
 // 6.84 TB/s with Philox against 5.86 for the 4-lanes-per-row persistent walk.  Measured
 // (profiles/r02_ab_flat.txt, same box): C4g 0.767 -> 0.842, C4r 0.781 -> 0.911 of the HBM
 // peak with the prefetch (0.81 / 0.79 without it; 2 quads per batch / 3 CTAs/SM lose).
-// Griewank (the heaviest fitness fold, phase 2) measured best with more CTAs/SM and only the
-// contiguous X/V tile prefetched: C4g 0.842 -> 0.874 (C4r loses 5 points with the same).
+// Per-problem knobs (measurement builds).  With x' folded in phase 2, Griewank measured best
+// with 6 CTAs/SM and only X/V prefetched (0.874); since the flat phase computes its terms
+// (pre_quad) the common defaults win for it too (C4g 0.910, profiles/r02_ab_flat2.txt).
 template <int P>
 __host__ __device__ constexpr int flat_minb() { return P == GRIEWANK ? EVOX_FLAT_MINB_GRIEWANK : EVOX_FLAT_MINB; }
 template <int P>
@@ -390,13 +378,15 @@ template <int P, class G, bool UNI>
 __global__ void __launch_bounds__(256, flat_minb<P>()) k_pso_gen_flat(PsoArgs a) {
     static_assert(G::WPR == 1, "flat phase: warp-row geometries only");
     extern __shared__ __align__(128) unsigned char flat_smem_buf[];
-    float4* xs = reinterpret_cast<float4*>(flat_smem_buf);  // [RPC][NQ] staged x' (+ [ld] htab)
+    float4* st = reinterpret_cast<float4*>(flat_smem_buf);  // staged tile (+ [ld] htab)
     __shared__ Fit<P> sh_acc[1];
     __shared__ float sh_head[1];
     __shared__ unsigned char sh_pend[G::RPC];
     __shared__ unsigned long long sh_k[WARPS];
     const int NQ = (int)(a.ld >> 2);
-    const float* htab = HTable<P, G>::fill(reinterpret_cast<float*>(xs + G::RPC * NQ), a.ld);
+    const int tq = G::RPC * NQ;  // staged quads per component
+    const float* htab =
+        HTable<P, G>::fill(reinterpret_cast<float*>(st + tq * stage_comps<P>()), a.ld);
     const RowMap<G> m(NQ);
     const long long row0 = (long long)blockIdx.x * G::RPC;
     const int nrow = a.rows - row0 < G::RPC ? (int)(a.rows - row0) : G::RPC;
@@ -456,7 +446,7 @@ __global__ void __launch_bounds__(256, flat_minb<P>()) k_pso_gen_flat(PsoArgs a)
                 mv.x[0] = x[k];
                 mv.v[0] = v[k];
                 mv.p[0] = p[k];
-                xs[i] = mv.step(0, q);
+                stage_quad<P>(st, tq, i, q, mv.step(0, q), htab);
             }
         }
     }
@@ -464,14 +454,8 @@ __global__ void __launch_bounds__(256, flat_minb<P>()) k_pso_gen_flat(PsoArgs a)
     // phase 2: the geometry's fitness fold over the staged rows, tell, argmin key
     unsigned long long best = ~0ull;
     {
-        MoverSmem ms;
-        ms.xr = xs + (ok ? row - row0 : 0) * NQ;
-        Fit<P> acc;
-        float hx, tx;
-        bool tv;
-        NoPrefetch pf;
-        walk_segment<P, G>(ms, 0, NQ, a.D, ok, acc, hx, tx, tv, pf, htab);
-        const float f = reduce_row<P, G>(acc, a.D, hx, tx, tv, sh_acc, sh_head);
+        const float f = fold_staged_row<P, G>(st, tq, ok ? (int)(row - row0) : 0, NQ, a.D, ok,
+                                              htab, sh_acc, sh_head);
         if (m.leader && ok) {
             const bool imp = f < pf_old;  // per-row tell (A11): strict, NaN never improves
             a.f[row] = f;
@@ -489,10 +473,6 @@ __global__ void __launch_bounds__(256, flat_minb<P>()) k_pso_gen_flat(PsoArgs a)
         for (int i = 1; i < WARPS; ++i) k = sh_k[i] < k ? sh_k[i] : k;
         if (k != ~0ull) atomicMin(&a.ctl->gen_key, k);
     }
-}
-
-inline size_t flat_smem(int problem, long long ld, int rpc) {
-    return (size_t)rpc * (size_t)ld * 4 + (problem == GRIEWANK ? (size_t)ld * 4 : 0);
 }
 
 // Copy `n` quads src -> dst with this grid's threads, 4 float4 loads in flight per thread.
@@ -1170,8 +1150,11 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
         EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
             if constexpr (G_::WPR == 1 && G_::LPR <= 8) {
                 // short rows: flat tile walk + the geometry's fitness fold (bitwise k_pso_gen)
-                e = launch_pdl(k_pso_gen_flat<P_, G_, U_>, grid, a, st,
-                               flat_smem(problem, a.ld, G_::RPC));
+                const size_t smem = flat_stage_bytes<P_>(G_::RPC, a.ld);
+                if (smem > 48 * 1024)
+                    cudaFuncSetAttribute(k_pso_gen_flat<P_, G_, U_>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                e = launch_pdl(k_pso_gen_flat<P_, G_, U_>, grid, a, st, smem);
             } else {
                 using GW_ = Geom<G_::LPR, G_::WPR, G_::WPR == 1 ? EVOX_WAVE_U : EVOX_ROW_U, G_::EFL>;
                 e = launch_pdl(k_pso_gen_wave<P_, GW_, U_>, grid, a, st);

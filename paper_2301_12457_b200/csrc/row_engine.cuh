@@ -391,6 +391,77 @@ struct MoverEval {
 };
 
 // ---------------------------------------------------------------------------
+// Flat-tile kernels (k_pso_gen_flat, k_de_gen_flat, k_cso_gen_flat): a CTA moves the quads of
+// a tile of rows as one flat range, stages per-quad values in shared memory, then folds each
+// row's fitness in the row geometry's order (bitwise the row-walk kernels' f).
+//   staged layout: A[T][NQ] float4 (+ B[T][NQ] when pre_comps<P>() == 2), then htab.
+// Rosenbrock stages x' and is folded by the row engine (pairs straddle quads); the other
+// problems stage pre_quad's values (every expensive per-element term, computed by all 256
+// threads in the flat phase) and a lane only applies fold_quad's accumulator operations.
+struct MoverSmem {
+    const float4* xr;
+    float4 x[U];
+    template <bool EF>
+    __device__ __forceinline__ void load(int u, int q) { x[u] = xr[q]; }
+    template <bool EF>
+    __device__ __forceinline__ void load_late(int, int) {}
+    __device__ __forceinline__ float4 step(int u, int) { return x[u]; }
+};
+
+template <int P>
+__host__ __device__ constexpr int stage_comps() { return P == ROSENBROCK ? 1 : pre_comps<P>(); }
+
+// Bytes of staging for T rows of ld floats (+ the Griewank column table).
+template <int P>
+inline size_t flat_stage_bytes(long long T, long long ld) {
+    return (size_t)T * (size_t)ld * 4 * stage_comps<P>() + (P == GRIEWANK ? (size_t)ld * 4 : 0);
+}
+
+// Stage quad i (column quad q) of the tile.
+template <int P>
+__device__ __forceinline__ void stage_quad(float4* st, int tile_quads, int i, int q, float4 x,
+                                           const float* htab) {
+    if constexpr (P == ROSENBROCK) {
+        st[i] = x;
+    } else {
+        float4 A, B;
+        pre_quad<P>(x, 4 * q, htab, A, B);
+        st[i] = A;
+        if constexpr (pre_comps<P>() == 2) st[tile_quads + i] = B;
+    }
+}
+
+// Fold staged row `lr` of the tile in geometry G's order (a lane group of LPR lanes per row,
+// WPR == 1); returns f in sub-lane 0.  Every lane of the warp must call it (shuffles).
+template <int P, class G>
+__device__ __forceinline__ float fold_staged_row(const float4* st, int tile_quads, int lr, int NQ,
+                                                 long long D, bool row_ok, const float* htab,
+                                                 Fit<P>* sh_acc, float* sh_head) {
+    static_assert(G::WPR == 1, "warp-row geometries only");
+    Fit<P> acc;
+    float hx = 0.f, tx = 0.f;
+    bool tv = false;
+    if constexpr (P == ROSENBROCK) {
+        MoverSmem ms;
+        ms.xr = st + lr * NQ;
+        NoPrefetch pf;
+        walk_segment<P, G>(ms, 0, NQ, D, row_ok, acc, hx, tx, tv, pf, htab);
+    } else {
+        const int sl = lane_id() & (G::LPR - 1);
+        if (row_ok) {
+            const float4* A = st + lr * NQ;
+            const float4* B = st + tile_quads + lr * NQ;
+            for (int q = sl; q < NQ; q += G::LPR) {
+                const float4 a = A[q];
+                const float4 b = pre_comps<P>() == 2 ? B[q] : a;
+                fold_quad<P>(acc, a, b, 4 * q, (int)D);
+            }
+        }
+    }
+    return reduce_row<P, G>(acc, D, hx, tx, tv, sh_acc, sh_head);
+}
+
+// ---------------------------------------------------------------------------
 // Grid-level argmin + finalize (A12/A13).
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long k) {
 #pragma unroll
