@@ -341,6 +341,9 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : EVOX_WAVE_MI
 #ifndef EVOX_FLAT_PF
 #define EVOX_FLAT_PF 3  // bulk L2 prefetch of the CTA's tile at its start: bit 0 X, V; bit 1 P rows
 #endif
+#ifndef EVOX_FLAT_G32
+#define EVOX_FLAT_G32 0  // warp-per-row rows also take k_pso_gen_flat (tiles of 8 rows)
+#endif
 #ifndef EVOX_FLAT_PF_GRIEWANK
 #define EVOX_FLAT_PF_GRIEWANK EVOX_FLAT_PF
 #endif
@@ -415,8 +418,8 @@ __global__ void __launch_bounds__(256, flat_minb<P>()) k_pso_gen_flat(PsoArgs a)
     float pf_old = 0.0f;
     if (m.leader && ok) pf_old = a.pf[row];
     __syncthreads();
-    // phase 1: flat walk of the tile (r = i / NQ exactly: i < 2^11, NQ <= 64)
-    const uint32_t magic = (1u << 20) / (uint32_t)NQ + 1u;
+    // phase 1: flat walk of the tile (r = i / NQ exactly: i * NQ < 2^32)
+    const uint32_t magic = (uint32_t)(0xffffffffu / (uint32_t)NQ) + 1u;
     constexpr int K = EVOX_FLAT_K;
     for (int b = 0; b < n; b += 256 * K) {
         float4 x[K], v[K], p[K];
@@ -432,7 +435,7 @@ __global__ void __launch_bounds__(256, flat_minb<P>()) k_pso_gen_flat(PsoArgs a)
         for (int k = 0; k < K; ++k) {
             const int i = b + 256 * k + (int)threadIdx.x;
             if (i < n) {
-                const int r = (int)(((uint32_t)i * magic) >> 20);
+                const int r = (int)__umulhi((uint32_t)i, magic);
                 if (!sh_pend[r]) p[k] = ld_stream<EVOX_FLAT_EF != 0>(Pt + i);
             }
         }
@@ -440,7 +443,7 @@ __global__ void __launch_bounds__(256, flat_minb<P>()) k_pso_gen_flat(PsoArgs a)
         for (int k = 0; k < K; ++k) {
             const int i = b + 256 * k + (int)threadIdx.x;
             if (i < n) {
-                const int r = (int)(((uint32_t)i * magic) >> 20);
+                const int r = (int)__umulhi((uint32_t)i, magic);
                 const int q = i - r * NQ;
                 MoverPso<UNI, false> mv(a, row0 + r, (uint32_t)t, sh_pend[r] != 0);
                 mv.x[0] = x[k];
@@ -1148,7 +1151,7 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
         // the wave kernel keeps fewer chunks in flight (registers for 3 CTAs/SM); the chunk
         // count never changes a lane's quad order, so the reduction order is the geometry's
         EVOX_DISPATCH_UNI(a.uniform_bounds, EVOX_DISPATCH_PROB(problem, EVOX_DISPATCH_GEOM(a.ld, {
-            if constexpr (G_::WPR == 1 && G_::LPR <= 8) {
+            if constexpr (G_::WPR == 1 && (G_::LPR <= 8 || EVOX_FLAT_G32)) {
                 // short rows: flat tile walk + the geometry's fitness fold (bitwise k_pso_gen)
                 const size_t smem = flat_stage_bytes<P_>(G_::RPC, a.ld);
                 if (smem > 48 * 1024)
