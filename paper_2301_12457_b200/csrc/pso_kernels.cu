@@ -270,6 +270,10 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : (G::LPR == 4
 #ifndef EVOX_ROW_U
 #define EVOX_ROW_U 3  // chunks in flight of the wave kernel, CTA-per-row geometry
 #endif
+#ifndef EVOX_WAVE_PF
+#define EVOX_WAVE_PF 3  // warp-row wave kernel: L2 prefetch of the CTA's rows (bit 0 X, V; bit 1 P):
+                        // H 0.935 -> 0.974, H-sphere 0.969 -> 0.989 (profiles/r02_ab_wave_pf.txt)
+#endif
 #ifndef EVOX_WAVE_U
 #define EVOX_WAVE_U 2  // chunks in flight per lane group in the wave kernel (warp-row geometries)
 #endif
@@ -299,6 +303,18 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : EVOX_WAVE_MI
     pdl_launch_dependents();
     const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
     const bool pend = ok ? a.imp[row] != 0 : true;
+#if EVOX_WAVE_PF
+    if constexpr (G::WPR == 1) {
+        // the CTA's rows HBM -> L2 at its start (X, V contiguous; P per row unless pending)
+        const long long r0 = (long long)blockIdx.x * G::RPC;
+        const long long nr = a.rows - r0 < G::RPC ? a.rows - r0 : G::RPC;
+        if ((EVOX_WAVE_PF & 1) && threadIdx.x == 0 && nr > 0) {
+            prefetch_l2(a.X + r0 * a.ld, nr * a.ld * 4);
+            prefetch_l2(a.V + r0 * a.ld, nr * a.ld * 4);
+        }
+        if ((EVOX_WAVE_PF & 2) && m.leader && ok && !pend) prefetch_l2(a.P + row * a.ld, a.ld * 4);
+    }
+#endif
     float pf_old = 0.0f;
     if (m.leader && ok) pf_old = a.pf[row];
     unsigned long long best = ~0ull;
@@ -1103,6 +1119,9 @@ bool pso_prefetch_next(long long ld, long long rows) {
     return !(geom_id(ld) == 1 && rows * ld > BIG);
 }
 
+#ifndef EVOX_WAVE_GRIEWANK
+#define EVOX_WAVE_GRIEWANK 0  // measurement builds: Griewank's warp-per-row rows on the wave grid
+#endif
 #ifndef EVOX_WAVE
 // which big populations take the wave grid (bit k: geometry id k; measurement builds may
 // change it).  Measured same box (profiles/r02_ab_wave_h.txt): warp-per-row rows with 2 chunks
@@ -1118,7 +1137,7 @@ bool pso_wave(int problem, long long ld, long long rows) {
     if (g == 0 || g == 3) return true;  // short rows: k_pso_gen_flat
     // Griewank's warp-row kernels keep a 16 KB shared-memory column table per CTA: at 4 CTAs/SM
     // that takes the L1 the streaming loads need (0.874 -> 0.801): persistent grid
-    return !(problem == GRIEWANK && g == 1);
+    return !(problem == GRIEWANK && g == 1 && !EVOX_WAVE_GRIEWANK);
 }
 
 int pso_gen_grid(int problem, long long ld, long long rows, int device, bool wave) {
