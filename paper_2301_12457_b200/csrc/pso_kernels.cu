@@ -641,11 +641,68 @@ __global__ void __launch_bounds__(256) k_pso_fin(PsoArgs a, long long t_arg) {
 // count for short rows (a lane's quad order, hence every reduction order, is unchanged).
 #define EVOX_PSO_GEOM(G_) Geom<G_::LPR, G_::WPR, G_::LPR <= 8 ? EVOX_PSO_SHORT_U : G_::NU, G_::EFL>
 
+// The cooperative kernel's partial last round ("tail"): rows [rw, rows) are fewer than the
+// grid's row slots, so instead of a few warps walking one more whole row each while the rest of
+// the grid waits at the barrier, every CTA takes <= TR of them as one flat tile (the phases of
+// k_pso_gen_flat: all 256 threads move the tile's quads and stage their fitness pre-terms, then
+// the geometry's lane groups fold each row in the geometry's order -- bitwise the row walk).
+// Called by every thread of the CTA (CTA-local barriers); returns this thread's argmin key.
+template <int P, class G, bool UNI>
+__device__ __forceinline__ unsigned long long pso_tail_tile(const PsoArgs& a, long long row0,
+                                                            int nrow, unsigned long long t,
+                                                            float4* st, const float* htab,
+                                                            Fit<P>* sh_acc, float* sh_head,
+                                                            unsigned char* sh_pend) {
+    const int NQ = (int)(a.ld >> 2);
+    const int tq = nrow * NQ;
+    const int wid = threadIdx.x >> 5, lane = lane_id();
+    const int lr = wid * G::RPW + lane / G::LPR;  // this lane group's row in the tile
+    const bool ok = lr < nrow;
+    const bool lead = ok && (lane & (G::LPR - 1)) == 0;
+    if ((int)threadIdx.x < nrow) sh_pend[threadIdx.x] = a.imp[row0 + threadIdx.x];
+    float pf_old = 0.0f;
+    if (lead) pf_old = a.pf[row0 + lr];
+    __syncthreads();
+    const uint32_t magic = (uint32_t)(0xffffffffu / (uint32_t)NQ) + 1u;  // i / NQ exactly
+    const float4* Xt = reinterpret_cast<const float4*>(a.X) + row0 * NQ;
+    const float4* Vt = reinterpret_cast<const float4*>(a.V) + row0 * NQ;
+    const float4* Pt = reinterpret_cast<const float4*>(a.P) + row0 * NQ;
+    for (int i = threadIdx.x; i < tq; i += 256) {
+        const int r = (int)__umulhi((uint32_t)i, magic);
+        const int q = i - r * NQ;
+        const bool pend = sh_pend[r] != 0;
+        MoverPso<UNI, true> mv(a, row0 + r, (uint32_t)t, pend);
+        mv.x[0] = ld_stream<G::EFL>(Xt + i);
+        mv.v[0] = ld_stream<G::EFL>(Vt + i);
+        if (!pend) mv.p[0] = ld_stream<G::EFL>(Pt + i);
+        stage_quad<P>(st, tq, i, q, mv.step(0, q), htab);
+    }
+    __syncthreads();
+    unsigned long long best = ~0ull;
+    if (wid * G::RPW < nrow) {  // warp-uniform: warps without rows skip the fold
+        const float f = fold_staged_row<P, G>(st, tq, ok ? lr : 0, NQ, a.D, ok, htab, sh_acc,
+                                              sh_head);
+        if (lead) {
+            const long long row = row0 + lr;
+            const bool imp = f < pf_old;  // per-row tell (A11): strict, NaN never improves
+            a.f[row] = f;
+            a.imp[row] = imp ? 1 : 0;
+            if (imp) a.pf[row] = f;
+            best = make_key(f, a.row0 + row);
+        }
+    }
+    __syncthreads();  // staging and sh_pend are reused next generation
+    return best;
+}
+
 #ifndef EVOX_MID_U
 #define EVOX_MID_U 4     // chunks in flight of the cooperative kernel, warp-per-row geometry
 #endif
 #ifndef EVOX_MID_MINB
 #define EVOX_MID_MINB EVOX_MINB  // its CTAs/SM (register cap), warp-per-row geometry
+#endif
+#ifndef EVOX_MID_TAIL
+#define EVOX_MID_TAIL 32768  // max staging bytes per CTA of the tail split (0: off)
 #endif
 #ifndef EVOX_MID_PF
 #define EVOX_MID_PF 1  // k_pso_run_mid: L2 prefetch of the next generation's first rows
@@ -661,11 +718,13 @@ __global__ void __launch_bounds__(256) k_pso_fin(PsoArgs a, long long t_arg) {
 template <int P, class G, bool UNI>
 __global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB
                                                    : (G::WPR == 1 ? EVOX_MID_MINB : EVOX_MINB))
-    k_pso_run_mid(PsoArgs a, long long n) {
+    k_pso_run_mid(PsoArgs a, long long n, long long rw, int tr) {
     __shared__ Fit<P> sh_acc[G::WPR];
     __shared__ float sh_head[G::WPR];
     __shared__ __align__(16) HStore<P, G> sh_h;
     __shared__ int sh_abort;
+    __shared__ unsigned char sh_pend[G::WPR == 1 ? G::RPC : 1];
+    extern __shared__ __align__(128) unsigned char mid_tail_smem[];  // tail staging (tr > 0)
     const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
     const RowMap<G> m(a.ld >> 2);
     Ctl* ctl = a.ctl;
@@ -673,8 +732,25 @@ __global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB
     // so every CTA reads the same base
     const unsigned int base = *(volatile unsigned int*)&ctl->bar;
     unsigned long long t = *(volatile unsigned long long*)&ctl->t;
+    // rows [0, rw) are walked by the warps' whole rounds; with tr > 0, rows [rw, rows) are the
+    // tail tiles, tr rows per CTA (pso_tail_tile)
+    PsoArgs aw = a;
+    aw.rows = rw;
     for (long long g = 0; g < n; ++g, ++t) {
-        const unsigned long long best = pso_gen_rows<P, G, UNI, true>(a, m, t, htab, sh_acc, sh_head);
+        unsigned long long best = pso_gen_rows<P, G, UNI, true>(aw, m, t, htab, sh_acc, sh_head);
+        if constexpr (G::WPR == 1) {
+            if (tr > 0) {
+                const long long row0 = rw + (long long)blockIdx.x * tr;
+                const long long left = a.rows - row0;
+                const int nrow = left < tr ? (left > 0 ? (int)left : 0) : tr;
+                if (nrow > 0) {  // CTA-uniform
+                    const unsigned long long k = pso_tail_tile<P, G, UNI>(
+                        a, row0, nrow, t, reinterpret_cast<float4*>(mid_tail_smem), htab, sh_acc,
+                        sh_head, sh_pend);
+                    best = k < best ? k : best;
+                }
+            }
+        }
 #if EVOX_MID_PF
         // the warp's first rows of the next generation (its own, already final) go to L2
         // while the grid drains the tail of this one (the pbest row only if not pending)
@@ -1215,11 +1291,32 @@ cudaError_t launch_pso_run_mid(int problem, const PsoArgs& a, long long n, cudaS
         using GM_ = Geom<G_::LPR, G_::WPR, G_::LPR == 32 && G_::WPR == 1 ? EVOX_MID_U : G_::NU,
                          G_::EFL>;
         const void* fn = (const void*)k_pso_run_mid<P_, GM_, U_>;
-        const int grid = grid_for(fn, row_units<G_>(a.rows), dev);  // resident grid only
+        // the tail split: the rows beyond the grid's whole rounds as flat tiles of <= tr rows
+        // per CTA, when their staging fits EVOX_MID_TAIL bytes (warp-row geometries)
+        size_t smem = 0;
+        long long rw = a.rows;
+        int tr = 0;
+        int grid = grid_for(fn, row_units<G_>(a.rows), dev);  // resident grid only
+        if (GM_::WPR == 1 && EVOX_MID_TAIL > 0) {
+            const long long slots = (long long)grid * GM_::RPC;  // rows per round of the grid
+            const long long full = a.rows / slots * slots;
+            const long long tail = a.rows - full;
+            const long long t_r = (tail + grid - 1) / grid;
+            const size_t bytes = (size_t)t_r * (size_t)a.ld * 4 * stage_comps<P_>();
+            if (tail > 0 && t_r <= GM_::RPC && bytes <= (size_t)EVOX_MID_TAIL) {
+                int per_sm = 1;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, bytes);
+                if ((long long)per_sm * sm_count(dev) >= grid) {  // still co-resident
+                    rw = full;
+                    tr = (int)t_r;
+                    smem = bytes;
+                }
+            }
+        }
         PsoArgs aa = a;
         long long nn = n;
-        void* args[] = {&aa, &nn};
-        e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(256), args, 0, st);
+        void* args[] = {&aa, &nn, &rw, &tr};
+        e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(256), args, smem, st);
     })));
     return e != cudaSuccess ? e : cudaGetLastError();
 }

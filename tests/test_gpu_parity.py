@@ -228,6 +228,26 @@ def test_pso_wave_kernel_equals_persistent(problem, N, D):
     b.close()
 
 
+@pytest.mark.parametrize("problem,N,D", [("ackley", 340_001, 100), ("rosenbrock", 140_000, 250),
+                                         ("griewank", 400_000, 90)])
+def test_pso_flat_kernel_per_dimension_bounds(problem, N, D):
+    """The flat-tile kernel with per-column bounds (the non-uniform-bounds instantiation) is
+    bitwise the persistent row walk, and every position stays inside its column's box."""
+    lo, hi = WL.BOUNDS[problem]
+    lb = np.linspace(lo, lo / 4, D).astype(np.float32)
+    ub = np.linspace(hi / 3, hi, D).astype(np.float32)
+    a = ev.PSO(N, D, lb, ub, seed=5)
+    a.step(problem, 3)
+    b = ev.PSO(N, D, lb, ub, seed=5, flags=E.FLAG_NO_WAVE)
+    b.step(problem, 3)
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
+        assert np.array_equal(ga[k], gb[k]), k
+    assert (ga["X"] >= lb).all() and (ga["X"] <= ub).all()
+    a.close()
+    b.close()
+
+
 def test_pso_wave_kernel_peer_group():
     """The wave grid with the in-kernel peer exchange (k_pso_fin runs it), W = 2 ranks of
     4e7 elements each (CTA-per-row geometry), bitwise the single-shard persistent run."""
