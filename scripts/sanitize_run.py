@@ -27,6 +27,16 @@ for D in (10, 100, 1003, 4099):
 pso = ev.PSO(300, 1000, -5, 5, seed=2, flags=ev.evox.FLAG_NO_SMALL | ev.evox.FLAG_NO_MID)
 pso.step("ackley", 3)                    # multi-CTA generation kernel + grid argmin
 pso.best()
+for p, N, D in (("griewank", 340_000, 100), ("rosenbrock", 140_000, 250), ("ackley", 34_000, 1000)):
+    pso = ev.PSO(N, D, -5, 5, seed=2)    # > 2^25 elements: flat tiles (short rows) / wave grid + prefetch
+    pso.step(p, 2)
+    pso.best()
+    pso.close()
+for p in ("sphere", "ackley", "rosenbrock"):
+    pso = ev.PSO(3001, 1000, -5, 5, seed=2)  # cooperative kernel with the flat tail tiles
+    pso.step(p, 3)
+    pso.best()
+    pso.close()
 pso = ev.PSO(8200, 4100, -5, 5, seed=2)  # > 2^25 elements, CTA-per-row: wave grid + k_pso_fin
 pso.step("rosenbrock", 2)
 pso.best()
