@@ -551,7 +551,7 @@ struct evox_pso : Base {
 namespace {
 
 bool pso_use_wave(const evox_pso* s, int problem) {
-    return !(s->flags & EVOX_FLAG_NO_WAVE) && evox::pso_wave(problem, s->ld, s->rows);
+    return !(s->flags & EVOX_FLAG_NO_WAVE) && evox::pso_wave(problem, s->ld, s->rows, s->device);
 }
 
 void pso_layout(evox_pso* s, Carver& c) {

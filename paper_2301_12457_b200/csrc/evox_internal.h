@@ -137,7 +137,7 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
 // whose PsoArgs.fin_kernel is set; t_new < 0: the index ctl->t + 1.
 cudaError_t launch_pso_fin(const PsoArgs& a, long long t_new, cudaStream_t st);
 // Big populations take the wave grid (k_pso_gen_wave + k_pso_fin) unless no_wave.
-bool pso_wave(int problem, long long ld, long long rows);
+bool pso_wave(int problem, long long ld, long long rows, int device);
 // Mode-A next-row L2 prefetch of the PSO generation (PsoArgs.pf_next): a schedule choice
 // measured per geometry and size, never a change of any result bit.
 bool pso_prefetch_next(long long ld, long long rows);

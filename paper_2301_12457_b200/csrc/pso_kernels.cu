@@ -274,6 +274,9 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : (G::LPR == 4
 #define EVOX_WAVE_PF 3  // warp-row wave kernel: L2 prefetch of the CTA's rows (bit 0 X, V; bit 1 P):
                         // H 0.935 -> 0.974, H-sphere 0.969 -> 0.989 (profiles/r02_ab_wave_pf.txt)
 #endif
+#ifndef EVOX_WAVE_PF_MAX_LD
+#define EVOX_WAVE_PF_MAX_LD 1024
+#endif
 #ifndef EVOX_WAVE_U
 #define EVOX_WAVE_U 2  // chunks in flight per lane group in the wave kernel (warp-row geometries)
 #endif
@@ -304,7 +307,10 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : EVOX_WAVE_MI
     const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
     const bool pend = ok ? a.imp[row] != 0 : true;
 #if EVOX_WAVE_PF
-    if constexpr (G::WPR == 1) {
+    // only while the grid's tiles fit L2 comfortably: 8 rows x ld x 12 B on ~600 resident CTAs
+    // is 58 MB at ld = 1024; at dim 1500 / 2048 / 4096 the prefetch thrashes L2 (0.85 / 0.76 /
+    // 0.61-0.76 against 0.88 / 0.83 / 0.72-0.94 without, profiles/r02_wave_threshold.txt)
+    if (G::WPR == 1 && a.ld <= EVOX_WAVE_PF_MAX_LD) {
         // the CTA's rows HBM -> L2 at its start (X, V contiguous; P per row unless pending)
         const long long r0 = (long long)blockIdx.x * G::RPC;
         const long long nr = a.rows - r0 < G::RPC ? a.rows - r0 : G::RPC;
@@ -1195,6 +1201,9 @@ bool pso_prefetch_next(long long ld, long long rows) {
     return !(geom_id(ld) == 1 && rows * ld > BIG);
 }
 
+#ifndef EVOX_WAVE_MIN_WAVES
+#define EVOX_WAVE_MIN_WAVES 3  // minimum waves of CTAs for the warp-per-row wave grid
+#endif
 #ifndef EVOX_WAVE_GRIEWANK
 #define EVOX_WAVE_GRIEWANK 0  // measurement builds: Griewank's warp-per-row rows on the wave grid
 #endif
@@ -1207,9 +1216,19 @@ bool pso_prefetch_next(long long ld, long long rows) {
 // C4r 0.781 -> 0.911).
 #define EVOX_WAVE ((1 << 0) | (1 << 1) | (1 << 2) | (1 << 3))
 #endif
-bool pso_wave(int problem, long long ld, long long rows) {
+bool pso_wave(int problem, long long ld, long long rows, int device) {
     const int g = geom_id(ld);
     if (rows * ld <= BIG || !((EVOX_WAVE >> g) & 1)) return false;
+    // warp-per-row rows: the wave grid pays off only over enough waves of CTAs -- with few
+    // (pop 1e4 x dim 4096: 1,250 CTAs of 8 rows on 592 slots = 2.1 waves: 0.72 vs 0.79; dim 3000
+    // at 2.5 waves 0.74 vs 0.76; dim 2048 at 4.2 waves 0.83 vs 0.80) its last partial wave idles
+    // most of the GPU, where the persistent walk spreads the rows over its warps.  The flat and
+    // CTA-per-row grids win from 4.5 waves down (profiles/r02_wave_threshold.txt).
+    if (g == 1) {
+        const long long units = (rows + 7) / 8;
+        const long long slots = (long long)sm_count(device) * EVOX_WAVE_MINB;
+        if (units < (long long)EVOX_WAVE_MIN_WAVES * slots) return false;
+    }
     if (g == 0 || g == 3) return true;  // short rows: k_pso_gen_flat
     // Griewank's warp-row kernels keep a 16 KB shared-memory column table per CTA: at 4 CTAs/SM
     // that takes the L1 the streaming loads need (0.874 -> 0.801): persistent grid
