@@ -55,7 +55,8 @@ def gen_kernel_name(cfg, rows, world):
         return f"k_pso_run_mid<{cfg.problem}>"
     if cfg.algo == "pso" and n > (1 << 25) and ld <= 256:
         return f"k_pso_gen_flat<{cfg.problem}>"
-    if cfg.algo == "pso" and n > (1 << 25) and (ld > 4096 or (ld > 256 and cfg.problem != "griewank")):
+    if cfg.algo == "pso" and n > (1 << 25) and (ld > 4096 or (
+            ld > 256 and cfg.problem != "griewank" and (rows + 7) // 8 >= 3 * 148 * 4)):
         return f"k_pso_gen_wave<{cfg.problem}>"
     if cfg.algo == "de" and ld <= 256:
         return f"k_de_gen_flat<{cfg.problem}>"
