@@ -103,8 +103,9 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
     if constexpr ((EVOX_EF & 1) != 0 && EF) return __ldcs(p);
     else return *p;
 }
+template <bool EF = true>
 __device__ __forceinline__ void st_stream(float4* p, float4 v) {
-    if constexpr ((EVOX_EF & 2) != 0) __stcs(p, v);
+    if constexpr ((EVOX_EF & 2) != 0 && EF) __stcs(p, v);
     else *p = v;
 }
 

@@ -17,7 +17,9 @@ namespace {
 // PSO move of one row (A1, A3, A4, lazy A5).  Holds a reference to the kernel
 // parameter block (resolved to constant-bank operands once inlined: the
 // Philox round keys, w, phi*2^-24 and the bounds feed instructions directly).
-template <bool UNI, bool G_COHERENT = false>
+// STS: evict-first stores (the row-walk kernels); the kernels that bulk-prefetch their tile into
+// L2 store (and load) with the default policy (profiles/r02_ab_hints.txt).
+template <bool UNI, bool G_COHERENT = false, bool STS = true>
 struct MoverPso {
     const PsoArgs& a;
     float4* Xr;
@@ -48,7 +50,7 @@ struct MoverPso {
     __device__ __forceinline__ float4 step(int u, int q) {
         const float4 xo = x[u];
         const float4 pb = pend ? xo : p[u];
-        if (pend) st_stream(Pr + q, xo);
+        if (pend) st_stream<STS>(Pr + q, xo);
         // G is read-only for a generation kernel (non-coherent path); the persistent
         // kernels rewrite it between generations: a plain (coherent, L1-cached) load,
         // ordered after the rewrite by the barrier's acquire + bar.sync.
@@ -74,8 +76,8 @@ struct MoverPso {
         pso_elem(xn.z, vn.z, pb.z, g.z, scaled_u24(b1.z, cp), scaled_u24(b2.z, cg), w, lo.z, hi.z);
         pso_elem(xn.w, vn.w, pb.w, g.w, scaled_u24(b1.w, cp), scaled_u24(b2.w, cg), w, lo.w, hi.w);
         zero_pad(xn, vn, q, a.D);
-        st_stream(Xr + q, xn);
-        st_stream(Vr + q, vn);
+        st_stream<STS>(Xr + q, xn);
+        st_stream<STS>(Vr + q, vn);
         return xn;
     }
 };
@@ -274,6 +276,9 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : (G::LPR == 4
 #define EVOX_WAVE_PF 3  // warp-row wave kernel: L2 prefetch of the CTA's rows (bit 0 X, V; bit 1 P):
                         // H 0.935 -> 0.974, H-sphere 0.969 -> 0.989 (profiles/r02_ab_wave_pf.txt)
 #endif
+#ifndef EVOX_WAVE_PF_EF
+#define EVOX_WAVE_PF_EF 0  // evict-first hints in the prefetching wave kernel (H: 0.963 with, 0.996 without)
+#endif
 #ifndef EVOX_WAVE_PF_MAX_LD
 #define EVOX_WAVE_PF_MAX_LD 1024
 #endif
@@ -291,7 +296,7 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : (G::LPR == 4
 // of a row waits on its imp flag; X and V of the row are already in flight by then
 // (walk_segment's late loads).  Micro (profiles/r02_micro_np3.txt): this schedule streams
 // the generation's access pattern at 6.48 TB/s against 6.13-6.33 for a persistent grid.
-template <int P, class G, bool UNI>
+template <int P, class G, bool UNI, bool PF>
 __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : EVOX_WAVE_MINB)
     k_pso_gen_wave(PsoArgs a) {
     __shared__ Fit<P> sh_acc[G::WPR];
@@ -306,11 +311,11 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : EVOX_WAVE_MI
     pdl_launch_dependents();
     const unsigned long long t = *(volatile unsigned long long*)&a.ctl->t;
     const bool pend = ok ? a.imp[row] != 0 : true;
-#if EVOX_WAVE_PF
-    // only while the grid's tiles fit L2 comfortably: 8 rows x ld x 12 B on ~600 resident CTAs
-    // is 58 MB at ld = 1024; at dim 1500 / 2048 / 4096 the prefetch thrashes L2 (0.85 / 0.76 /
-    // 0.61-0.76 against 0.88 / 0.83 / 0.72-0.94 without, profiles/r02_wave_threshold.txt)
-    if (G::WPR == 1 && a.ld <= EVOX_WAVE_PF_MAX_LD) {
+    // PF (chosen on the host only while the grid's tiles fit L2 comfortably: 8 rows x ld x 12 B
+    // on ~600 resident CTAs is 58 MB at ld = 1024; at dim 1500 / 2048 / 4096 the prefetch
+    // thrashes L2: 0.85 / 0.76 / 0.61-0.76 against 0.88 / 0.83 / 0.72-0.94 without,
+    // profiles/r02_wave_threshold.txt)
+    if constexpr (PF && G::WPR == 1) {
         // the CTA's rows HBM -> L2 at its start (X, V contiguous; P per row unless pending)
         const long long r0 = (long long)blockIdx.x * G::RPC;
         const long long nr = a.rows - r0 < G::RPC ? a.rows - r0 : G::RPC;
@@ -320,12 +325,11 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : EVOX_WAVE_MI
         }
         if ((EVOX_WAVE_PF & 2) && m.leader && ok && !pend) prefetch_l2(a.P + row * a.ld, a.ld * 4);
     }
-#endif
     float pf_old = 0.0f;
     if (m.leader && ok) pf_old = a.pf[row];
     unsigned long long best = ~0ull;
     if (m.wfirst < a.rows) {  // warp-uniform (CTA-uniform for WPR > 1)
-        MoverPso<UNI, false> mv(a, ok ? row : 0, (uint32_t)t, pend);
+        MoverPso<UNI, false, !(PF && !EVOX_WAVE_PF_EF)> mv(a, ok ? row : 0, (uint32_t)t, pend);
         Fit<P> acc;
         float hx, tx;
         bool tv;
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__(256, G::WPR > 1 ? EVOX_ROW_MINB : EVOX_WAVE_MI
 #define EVOX_FLAT_MINB 4  // its CTAs/SM (register cap)
 #endif
 #ifndef EVOX_FLAT_EF
-#define EVOX_FLAT_EF 1  // evict-first loads in the flat phase
+#define EVOX_FLAT_EF 0  // evict-first loads and stores in the flat phase (C4r: 0.892 with, 0.909 without)
 #endif
 #ifndef EVOX_FLAT_PF
 #define EVOX_FLAT_PF 3  // bulk L2 prefetch of the CTA's tile at its start: bit 0 X, V; bit 1 P rows
@@ -467,7 +471,7 @@ __global__ void __launch_bounds__(256, flat_minb<P>()) k_pso_gen_flat(PsoArgs a)
             if (i < n) {
                 const int r = (int)__umulhi((uint32_t)i, magic);
                 const int q = i - r * NQ;
-                MoverPso<UNI, false> mv(a, row0 + r, (uint32_t)t, sh_pend[r] != 0);
+                MoverPso<UNI, false, EVOX_FLAT_EF != 0> mv(a, row0 + r, (uint32_t)t, sh_pend[r] != 0);
                 mv.x[0] = x[k];
                 mv.v[0] = v[k];
                 mv.p[0] = p[k];
@@ -1272,9 +1276,13 @@ cudaError_t launch_pso_gen(int problem, const PsoArgs& a, int grid, cudaStream_t
                     cudaFuncSetAttribute(k_pso_gen_flat<P_, G_, U_>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 e = launch_pdl(k_pso_gen_flat<P_, G_, U_>, grid, a, st, smem);
+            } else if (G_::WPR == 1 && EVOX_WAVE_PF && a.ld <= EVOX_WAVE_PF_MAX_LD) {
+                // tile prefetch; default-policy loads and stores (the prefetched lines stay in L2)
+                using GWP_ = Geom<G_::LPR, 1, EVOX_WAVE_U, (EVOX_WAVE_PF_EF != 0)>;
+                e = launch_pdl(k_pso_gen_wave<P_, GWP_, U_, true>, grid, a, st);
             } else {
                 using GW_ = Geom<G_::LPR, G_::WPR, G_::WPR == 1 ? EVOX_WAVE_U : EVOX_ROW_U, G_::EFL>;
-                e = launch_pdl(k_pso_gen_wave<P_, GW_, U_>, grid, a, st);
+                e = launch_pdl(k_pso_gen_wave<P_, GW_, U_, false>, grid, a, st);
             }
         })));
         return e != cudaSuccess ? e : cudaGetLastError();
