@@ -3,7 +3,7 @@
 #   bash scripts/gpu_ncu_all.sh [tag]   -> gpurun_out/ncu_<tag>_<cfg>_raw.csv, launches_<tag>_H.csv
 tag=${1:-r02}
 mkdir -p gpurun_out
-for ck in H:k_pso_gen_wave C2:k_pso_run_mid C3:k_cso_gen C4g:k_pso_gen_flat C4r:k_pso_gen_flat \
+for ck in H:k_pso_gen_wave C3:k_cso_gen C4g:k_pso_gen_flat C4r:k_pso_gen_flat \
           C5:k_pso_gen_wave D1:k_de_gen_flat D2:k_de_gen EH-ackley:k_eval E5-griewank:k_eval; do
   c=${ck%%:*}; k=${ck#*:}
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
