@@ -203,6 +203,26 @@ def test_pso_mid_kernel_equals_stepwise(problem, N, D):
     assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
 
 
+@pytest.mark.parametrize("problem,N,D", [("ackley", 3001, 1000), ("rosenbrock", 3001, 100),
+                                         ("rastrigin", 700, 1001)])
+def test_pso_mid_tail_tiles_per_dimension_bounds(problem, N, D):
+    """The cooperative kernel's flat tail tiles with per-column bounds (non-uniform-bounds
+    instantiation) are bitwise one k_pso_gen launch per generation, inside every column's box."""
+    lo, hi = WL.BOUNDS[problem]
+    lb = np.linspace(lo, lo / 5, D).astype(np.float32)
+    ub = np.linspace(hi / 2, hi, D).astype(np.float32)
+    a = ev.PSO(N, D, lb, ub, seed=13)
+    a.step(problem, 6)
+    a.step(problem, 5)
+    b = ev.PSO(N, D, lb, ub, seed=13, flags=E.FLAG_NO_MID)
+    b.step(problem, 11)
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
+        assert np.array_equal(ga[k], gb[k]), k
+    assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
+    assert (ga["X"] >= lb).all() and (ga["X"] <= ub).all()
+
+
 @pytest.mark.parametrize("problem,N,D", [("ackley", 400, 100_000), ("rosenbrock", 2000, 17_001),
                                          ("griewank", 800, 50_000), ("ackley", 40_000, 1000),
                                          ("rosenbrock", 34_000, 1001), ("sphere", 9_000, 3999),
