@@ -417,6 +417,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--sustained-s", type=float, default=1.5,
+                    help="seconds of untimed generations before the sustained window (0: skip)")
     ap.add_argument("--pop", type=int, default=0, help="override the population (profiling only)")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
                     help="PSO winner exchange for N>1: in-kernel over NVLink peer memory "
@@ -537,6 +539,35 @@ def main():
     ms_total, k_avg_ms, fin_avg_ms = float(t[0]), float(t[1]), float(t[2])
     ms_per_step = ms_total / args.steps
 
+    # ---- sustained: the same K generations again after ~--sustained-s seconds of back-to-back
+    # (untimed) generations, once the board's power limit has set its steady SM clock: at H the
+    # 1000 W cap (sw_power_cap) takes the SM clock from ~1.9 GHz to ~1.56 GHz within ~0.5 s
+    # (profiles/r02_power_drift.txt).  Reported next to the headline window.
+    sus = None
+    if args.sustained_s > 0:
+        burn = int(min(5000, max(20, args.sustained_s * 1e3 / max(ms_per_step, 1e-3))))
+        h.step(cfg.problem, burn)
+        h.sync()
+        h.set_timing(True)
+        h.kernel_time(reset=True)
+        clocks2 = ClockSampler(local)
+        clocks2.start()
+        barrier()
+        e0.record(stream)
+        h.step(cfg.problem, args.steps)
+        e1.record(stream)
+        h.sync()
+        barrier()
+        clk2 = clocks2.stop()
+        k2_ms, k2_n, _ = h.kernel_time(reset=True)
+        h.set_timing(False)
+        t2 = torch.tensor([e0.elapsed_time(e1), k2_ms / max(k2_n, 1)], dtype=torch.float64,
+                          device=cdev)
+        if launched:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        sus = {"burn_in_generations": burn, "ms_per_step": float(t2[0]) / args.steps,
+               "kernel_ms": float(t2[1]), "clocks": clk2}
+
     # ---- end to end: one whole job through the public API with host buffers, timed by the
     # host clock (max over ranks): init from host lb/ub (H2D inside the C-ABI), X0 from the
     # seed, generation 0, then every step evox_*_step(1) + a synchronising best() D2H of the
@@ -571,7 +602,7 @@ def main():
         achieved = bytes_launch / (k_avg_ms * 1e-3) / 1e9
         kname = gen_kernel_name(cfg, rows, world)
         # the committed ncu entry is per generation of the kernel that actually runs
-        traffic = ncu_traffic(args.config + ("-mid" if "run_mid" in kname else ""))
+        traffic = ncu_traffic(args.config)
         gens_per_s = 1e3 / ms_per_step
         evaluated = cfg.pop * cfg.dim * (0.5 if cfg.algo == "cso" else 1.0)
         line = {
@@ -610,6 +641,16 @@ def main():
                                    "gbest publication" if peer else
                                    "gbest publication after the wave-grid generation kernel")}
                          if fin_launch else None),
+            "sustained": ({"value": 1e3 / sus["ms_per_step"], "unit": "generations/s",
+                           "ms_per_step": sus["ms_per_step"],
+                           "frac": bytes_launch / (sus["kernel_ms"] * 1e-3) / 1e9 / peak,
+                           "kernel_ms": sus["kernel_ms"],
+                           "burn_in_generations": sus["burn_in_generations"],
+                           "clocks": sus["clocks"],
+                           "note": "the same --steps generations timed the same way after "
+                                   "burn_in_generations untimed back-to-back generations, when "
+                                   "the board power limit has settled the SM clock"}
+                          if sus else None),
             "e2e": {"value": args.e2e_steps / e2e_s, "unit": "generations/s",
                     "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
                     "steps": args.e2e_steps,

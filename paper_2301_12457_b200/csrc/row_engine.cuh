@@ -55,6 +55,9 @@ namespace {
 #ifndef EVOX_ROW_MINB
 #define EVOX_ROW_MINB 3  // CTA-per-row geometry (ld > 4096): C5 0.872 -> 0.909 (r02_pf.txt)
 #endif
+#ifndef EVOX_PDL
+#define EVOX_PDL 1  // programmatic dependent launch of the generation kernels
+#endif
 #ifndef EVOX_AHEAD
 #define EVOX_AHEAD 4  // mode-B prefetch window, in lane groups
 #endif
@@ -638,7 +641,7 @@ inline cudaError_t launch_pdl(K kernel, int grid, const A& a, cudaStream_t st, s
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = EVOX_PDL;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, a);
