@@ -539,35 +539,6 @@ def main():
     ms_total, k_avg_ms, fin_avg_ms = float(t[0]), float(t[1]), float(t[2])
     ms_per_step = ms_total / args.steps
 
-    # ---- sustained: the same K generations again after ~--sustained-s seconds of back-to-back
-    # (untimed) generations, once the board's power limit has set its steady SM clock: at H the
-    # 1000 W cap (sw_power_cap) takes the SM clock from ~1.9 GHz to ~1.56 GHz within ~0.5 s
-    # (profiles/r02_power_drift.txt).  Reported next to the headline window.
-    sus = None
-    if args.sustained_s > 0:
-        burn = int(min(5000, max(20, args.sustained_s * 1e3 / max(ms_per_step, 1e-3))))
-        h.step(cfg.problem, burn)
-        h.sync()
-        h.set_timing(True)
-        h.kernel_time(reset=True)
-        clocks2 = ClockSampler(local)
-        clocks2.start()
-        barrier()
-        e0.record(stream)
-        h.step(cfg.problem, args.steps)
-        e1.record(stream)
-        h.sync()
-        barrier()
-        clk2 = clocks2.stop()
-        k2_ms, k2_n, _ = h.kernel_time(reset=True)
-        h.set_timing(False)
-        t2 = torch.tensor([e0.elapsed_time(e1), k2_ms / max(k2_n, 1)], dtype=torch.float64,
-                          device=cdev)
-        if launched:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        sus = {"burn_in_generations": burn, "ms_per_step": float(t2[0]) / args.steps,
-               "kernel_ms": float(t2[1]), "clocks": clk2}
-
     # ---- end to end: one whole job through the public API with host buffers, timed by the
     # host clock (max over ranks): init from host lb/ub (H2D inside the C-ABI), X0 from the
     # seed, generation 0, then every step evox_*_step(1) + a synchronising best() D2H of the
@@ -594,6 +565,36 @@ def main():
         dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     e2e_s, setup_s, steps_s, best_s, hist_s = (float(v) for v in e2e)
     e2e_h2d = 2 * 4 * cfg.dim / args.e2e_steps            # lb, ub (per job, amortised)
+    # ---- sustained (after the e2e job, on its handle, so the job is timed as before): the same
+    # K generations again after ~--sustained-s seconds of back-to-back (untimed) generations, once
+    # the board's power limit has set its steady SM clock: at H the 1000 W cap (sw_power_cap)
+    # takes the SM clock from ~1.9 GHz to ~1.56 GHz within ~0.5 s (DESIGN.md §7,
+    # profiles/r02_power_drift.txt).  Reported next to the headline window.
+    sus = None
+    if args.sustained_s > 0:
+        burn = int(min(5000, max(20, args.sustained_s * 1e3 / max(ms_per_step, 1e-3))))
+        h.step(cfg.problem, burn)
+        h.sync()
+        h.set_timing(True)
+        h.kernel_time(reset=True)
+        clocks2 = ClockSampler(local)
+        clocks2.start()
+        barrier()
+        e0.record(h.stream)
+        h.step(cfg.problem, args.steps)
+        e1.record(h.stream)
+        h.sync()
+        barrier()
+        clk2 = clocks2.stop()
+        k2_ms, k2_n, _ = h.kernel_time(reset=True)
+        h.set_timing(False)
+        t2 = torch.tensor([e0.elapsed_time(e1), k2_ms / max(k2_n, 1)], dtype=torch.float64,
+                          device=cdev)
+        if launched:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        sus = {"burn_in_generations": burn, "ms_per_step": float(t2[0]) / args.steps,
+               "kernel_ms": float(t2[1]), "clocks": clk2}
+
     e2e_d2h = (4 + 8 + 4 * cfg.dim) + 4 * len(hist) / args.e2e_steps
 
     if rank == 0:
