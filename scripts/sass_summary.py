@@ -31,14 +31,17 @@ def demangle(names):
 
 
 # the kernels the bench configs run (first matching instantiation of each family)
-want = [("k_pso_gen<1, evox::(anonymous namespace)::Geom<32, 1, 4, true>, true>", "H: k_pso_gen<ackley>, warp per row"),
-        ("k_pso_gen<4, evox::(anonymous namespace)::Geom<4, 1, 4, false>, true>", "C4r: k_pso_gen<rosenbrock>, 4 lanes per row"),
-        ("k_pso_gen_wave<1, evox::(anonymous namespace)::Geom<32, 8, 3, true>, true>", "C5: k_pso_gen_wave<ackley>, CTA per row"),
-        ("k_pso_run_mid<1, evox::(anonymous namespace)::Geom<32, 1, 4, true>, true>", "C2: k_pso_run_mid<ackley>"),
+want = [("k_pso_gen_wave<1, evox::(anonymous namespace)::Geom<32, 1, 2, false>, true, true>", "H: k_pso_gen_wave<ackley>, warp per row, tile prefetch"),
+        ("k_pso_gen_flat<4, evox::(anonymous namespace)::Geom<4, 1, 4, false>, true>", "C4r: k_pso_gen_flat<rosenbrock>, flat tiles of 64 rows"),
+        ("k_pso_gen_flat<3, evox::(anonymous namespace)::Geom<4, 1, 4, false>, true>", "C4g: k_pso_gen_flat<griewank>, flat tiles of 64 rows"),
+        ("k_pso_gen_wave<1, evox::(anonymous namespace)::Geom<32, 8, 3, true>, true, false>", "C5: k_pso_gen_wave<ackley>, CTA per row"),
+        ("k_pso_run_mid<1, evox::(anonymous namespace)::Geom<32, 1, 4, true>, true>", "C2: k_pso_run_mid<ackley> (+ tail tiles)"),
+        ("k_pso_gen<3, evox::(anonymous namespace)::Geom<32, 1, 4, true>, true>", "persistent row walk: k_pso_gen<griewank>, warp per row"),
         ("k_pso_gen_tma<1, true>", "opt-in: k_pso_gen_tma<ackley> (EVOX_FLAG_TMA)"),
         ("k_pso_fin(", "k_pso_fin (gbest publication / key-first exchange)"),
         ("k_cso_gen<2, evox::(anonymous namespace)::Geom<8, 1, 4, true>, true>", "C3: k_cso_gen<rastrigin>"),
-        ("k_de_gen<0, evox::(anonymous namespace)::Geom<4, 1, 2, false>, true>", "D1: k_de_gen<sphere>"),
+        ("k_de_gen_flat<0, evox::(anonymous namespace)::Geom<4, 1, 4, false>, true>", "D1: k_de_gen_flat<sphere>"),
+        ("k_de_gen<1, evox::(anonymous namespace)::Geom<32, 1, 4, true>, true>", "D2: k_de_gen<ackley>"),
         ("k_eval<1, evox::(anonymous namespace)::Geom<32, 1, 4, true> >", "EH: k_eval<ackley>")]
 dem = dict(zip(funcs, demangle(list(funcs))))
 classes = [("LDG.128", r"^LDG\.E(\.\w+)*\.128"), ("LDG.128 evict-first", r"^LDG\.E\.EF(\.\w+)*\.128"),
@@ -50,8 +53,8 @@ classes = [("LDG.128", r"^LDG\.E(\.\w+)*\.128"), ("LDG.128 evict-first", r"^LDG\
            ("total", r".")]
 print("# Static SASS of paper_2301_12457_b200/libevox.so (cuobjdump -sass), per kernel:")
 print("# instruction counts by class (mnemonic regex on the opcode).  Dynamic per-element cost at H")
-print("# (ncu smsp__inst_executed.sum, profiles/r02_ncu_full_H.txt): 1.956e9 warp instructions per")
-print("# launch x 32 lanes / 1e9 elements = 62.6 lane-instructions per element-generation.")
+print("# (ncu smsp__inst_executed.sum, profiles/r02_ncu_full_H.txt): 2.168e9 warp instructions per")
+print("# launch x 32 lanes / 1e9 elements = 69.4 lane-instructions per element-generation.")
 for key, label in want:
     hits = [f for f in funcs if key in dem[f]]
     if not hits:
