@@ -204,7 +204,8 @@ def test_pso_mid_kernel_equals_stepwise(problem, N, D):
 
 
 @pytest.mark.parametrize("problem,N,D", [("ackley", 3001, 1000), ("rosenbrock", 3001, 100),
-                                         ("rastrigin", 700, 1001)])
+                                         ("rastrigin", 700, 1001), ("griewank", 3001, 1000),
+                                         ("sphere", 2401, 257)])
 def test_pso_mid_tail_tiles_per_dimension_bounds(problem, N, D):
     """The cooperative kernel's flat tail tiles with per-column bounds (non-uniform-bounds
     instantiation) are bitwise one k_pso_gen launch per generation, inside every column's box."""
@@ -249,10 +250,12 @@ def test_pso_wave_kernel_equals_persistent(problem, N, D):
 
 
 @pytest.mark.parametrize("problem,N,D", [("ackley", 340_001, 100), ("rosenbrock", 140_000, 250),
-                                         ("griewank", 400_000, 90)])
+                                         ("griewank", 400_000, 90), ("ackley", 40_000, 1000),
+                                         ("rastrigin", 4_000, 9000)])
 def test_pso_flat_kernel_per_dimension_bounds(problem, N, D):
-    """The flat-tile kernel with per-column bounds (the non-uniform-bounds instantiation) is
-    bitwise the persistent row walk, and every position stays inside its column's box."""
+    """The flat-tile kernel and the wave kernels (warp per row with the tile prefetch, CTA per
+    row) with per-column bounds (the non-uniform-bounds instantiations) are bitwise the
+    persistent row walk, and every position stays inside its column's box."""
     lo, hi = WL.BOUNDS[problem]
     lb = np.linspace(lo, lo / 4, D).astype(np.float32)
     ub = np.linspace(hi / 3, hi, D).astype(np.float32)
