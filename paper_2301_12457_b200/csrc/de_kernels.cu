@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(256, EVOX_DE_FLAT_MINB) k_de_gen_flat(DeArgs a
     __shared__ int sh_jr[G::RPC];
     __shared__ float sh_fx[G::RPC];
     __shared__ unsigned char sh_si[G::RPC];
+    __shared__ float4* sh_out[G::RPC];  // the trial row (the other buffer)
     const int NQ = (int)(a.ld >> 2);
     const int tq = G::RPC * NQ;  // staged quads per component
     const float* htab =
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(256, EVOX_DE_FLAT_MINB) k_de_gen_flat(DeArgs a
         sh_jr[threadIdx.x] = (int)(((unsigned long long)jw.x * (unsigned long long)a.D) >> 32);
         sh_fx[threadIdx.x] = a.f[p][rw];
         sh_si[threadIdx.x] = (unsigned char)si;
+        sh_out[threadIdx.x] = reinterpret_cast<float4*>(a.buf[si ^ 1] + rw * a.ld);
     }
     __syncthreads();
     // phase 1: flat walk of the tile's trial quads (r = i / NQ exactly: i < 2^11, NQ <= 64)
@@ -297,9 +299,9 @@ __global__ void __launch_bounds__(256, EVOX_DE_FLAT_MINB) k_de_gen_flat(DeArgs a
         mv.Xa = sh_src[r][1];
         mv.Xb = sh_src[r][2];
         mv.Xc = sh_src[r][3];
-        mv.Out = reinterpret_cast<float4*>(a.buf[sh_si[r] ^ 1] + (row0 + r) * a.ld);
+        mv.Out = sh_out[r];
         mv.jrand = sh_jr[r];
-        mv.row_g = (uint32_t)(a.row0 + row0 + r);
+        mv.row_g = (uint32_t)(a.row0 + row0) + (uint32_t)r;
         mv.t = (uint32_t)t;
         mv.template load<G::EFL>(0, q);
         stage_quad<P>(st, tq, i, q, mv.step(0, q), htab);

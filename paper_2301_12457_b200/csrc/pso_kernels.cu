@@ -38,6 +38,10 @@ struct MoverPso {
         t = t_;
         pend = pend_;
     }
+    // row pointers already at hand (the flat tiles: tile base + r * NQ, 32-bit offsets)
+    __device__ __forceinline__ MoverPso(const PsoArgs& a_, float4* xr, float4* vr, float4* pr,
+                                        uint32_t row_g_, uint32_t t_, bool pend_)
+        : a(a_), Xr(xr), Vr(vr), Pr(pr), row_g(row_g_), t(t_), pend(pend_) {}
     template <bool EF>
     __device__ __forceinline__ void load(int u, int q) {
         x[u] = ld_stream<EF>(Xr + q);
@@ -471,7 +475,11 @@ __global__ void __launch_bounds__(256, flat_minb<P>()) k_pso_gen_flat(PsoArgs a)
             if (i < n) {
                 const int r = (int)__umulhi((uint32_t)i, magic);
                 const int q = i - r * NQ;
-                MoverPso<UNI, false, EVOX_FLAT_EF != 0> mv(a, row0 + r, (uint32_t)t, sh_pend[r] != 0);
+                const int o = i - q;  // r * NQ
+                MoverPso<UNI, false, EVOX_FLAT_EF != 0> mv(
+                    a, const_cast<float4*>(Xt) + o, const_cast<float4*>(Vt) + o,
+                    const_cast<float4*>(Pt) + o, (uint32_t)(a.row0 + row0) + (uint32_t)r,
+                    (uint32_t)t, sh_pend[r] != 0);
                 mv.x[0] = x[k];
                 mv.v[0] = v[k];
                 mv.p[0] = p[k];
@@ -681,7 +689,10 @@ __device__ __forceinline__ unsigned long long pso_tail_tile(const PsoArgs& a, lo
         const int r = (int)__umulhi((uint32_t)i, magic);
         const int q = i - r * NQ;
         const bool pend = sh_pend[r] != 0;
-        MoverPso<UNI, true> mv(a, row0 + r, (uint32_t)t, pend);
+        const int o = i - q;  // r * NQ
+        MoverPso<UNI, true> mv(a, const_cast<float4*>(Xt) + o, const_cast<float4*>(Vt) + o,
+                               const_cast<float4*>(Pt) + o, (uint32_t)(a.row0 + row0) + (uint32_t)r,
+                               (uint32_t)t, pend);
         mv.x[0] = ld_stream<G::EFL>(Xt + i);
         mv.v[0] = ld_stream<G::EFL>(Vt + i);
         if (!pend) mv.p[0] = ld_stream<G::EFL>(Pt + i);
