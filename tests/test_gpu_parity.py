@@ -500,6 +500,19 @@ def test_full_size_sampled_10_gens(cfg):
                                n_sample=64 if c.dim > 10_000 else 256)
 
 
+@pytest.mark.parametrize("cfg", ["C4g", "C4r", "H", "C2"])
+def test_full_size_sampled_100_gens(cfg):
+    """north_star's 100-generation comparison at the full-size configs, through the kernels the
+    bench times (flat tiles, the prefetching wave grid, the cooperative kernel): every one of
+    100 generations, sampled rows re-derived by the oracle from the GPU's pre-move state."""
+    c = WL.CONFIGS[cfg]
+    free, _ = torch.cuda.mem_get_info()
+    need = 3 * c.pop * WL.round4(c.dim) * 4 * 1.1
+    if need > free:
+        pytest.skip("not enough device memory")
+    _sampled_generations_check(c.problem, c.pop, c.dim, seed=3, gens=100, n_sample=96)
+
+
 def test_c2_full_parity_10_gens():
     """C2 (PSO/Ackley 1e4 x 1000) compared element by element every generation for 10
     generations (near-tie protocol R-9), checkpoints at 1 and 10."""
