@@ -154,6 +154,36 @@ def test_de_large_population_sampled():
     assert (f1 <= f0).all()
 
 
+@pytest.mark.parametrize("gens", [10, 100])
+def test_de_d1_sampled_generations(gens):
+    """D1 (DE/Sphere 1e6 x 100) through the flat-tile kernel the bench times: every generation,
+    sampled targets recomputed one by one by the oracle from the GPU's pre-generation
+    population (donors, crossover, greedy <= replacement; north_star 10 / 100 generations)."""
+    N, D, seed, p = 1_000_000, 100, 0, "sphere"
+    de = ev.DE(N, D, -5.12, 5.12, seed=seed)
+    de.step(p, 0)
+    rng = np.random.default_rng(1)
+    for t in range(gens):
+        X0 = de.view("X").cpu().numpy()[:, :D].copy()
+        f0 = de.view("F").cpu().numpy().copy()
+        de.step(p, 1)
+        X1 = de.view("X").cpu().numpy()[:, :D]
+        f1 = de.view("F").cpu().numpy()
+        for i in rng.integers(0, N, 16 if gens > 10 else 64):
+            r = O.de_indices(N, int(i), t, seed)
+            U = O.draw(1, D, int(i), t, 10, seed)[0]
+            u = O.de_trial_with(X0[i], X0[r[0]], X0[r[1]], X0[r[2]], U,
+                                O.de_jrand(D, int(i), t, seed), 0.5, 0.9, -5.12, 5.12)
+            fu = float(O.evaluate(p, u[None])[0])
+            if near_tie(fu, f0[i]):
+                continue
+            expect = u if fu <= f0[i] else X0[i]
+            assert np.array_equal(X1[i], expect), (t, i)
+        assert (f1 <= f0).all()
+        assert de.history()[-1] == f1.min()
+    de.close()
+
+
 def test_de_config_errors():
     with pytest.raises(E.ConfigError):
         ev.DE(3, 4, -1, 1)
