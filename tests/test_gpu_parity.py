@@ -598,9 +598,10 @@ def test_cso_nccl_path_single_rank():
     assert a.best()[:2] == b.best()[:2]
 
 
-def test_cso_c3_sampled_10_gens():
-    """C3 (CSO/Rastrigin 1e5 x 1000, B = pop/8): 10 generations; every generation sampled
-    pairs are recomputed one by one by the oracle from the GPU's pre-generation state
+@pytest.mark.parametrize("gens", [10, 100])
+def test_cso_c3_sampled_gens(gens):
+    """C3 (CSO/Rastrigin 1e5 x 1000, B = pop/8): 10 and 100 generations; every generation
+    sampled pairs are recomputed one by one by the oracle from the GPU's pre-generation state
     (winner bitwise unchanged, loser update bitwise, loser fitness within tolerance)."""
     c = WL.CONFIGS["C3"]
     lb, ub = WL.BOUNDS[c.problem]
@@ -608,7 +609,7 @@ def test_cso_c3_sampled_10_gens():
     cso = ev.CSO(c.pop, c.dim, lb, ub, block=B, seed=0)
     cso.step(c.problem, 0)
     rng = np.random.default_rng(0)
-    for t in range(10):
+    for t in range(gens):
         X0 = cso.view("X").cpu().numpy()[:, :c.dim].copy()
         V0 = cso.view("V").cpu().numpy()[:, :c.dim].copy()
         f0 = cso.view("F").cpu().numpy().copy()
@@ -620,7 +621,7 @@ def test_cso_c3_sampled_10_gens():
         assert changed.sum() <= c.pop // 2
         for blk in rng.choice(8, 2, replace=False):
             pairs = O.cso_pairs(B, int(blk), t, 0)
-            for a, b in pairs[rng.integers(0, len(pairs), 8)]:
+            for a, b in pairs[rng.integers(0, len(pairs), 8 if gens <= 10 else 2)]:
                 i, k = blk * B + a, blk * B + b
                 if near_tie(f0[i], f0[k]):
                     continue
