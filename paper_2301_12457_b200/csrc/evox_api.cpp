@@ -391,6 +391,7 @@ evox_status base_common_init(Base* b) {
     Ctl c;
     std::memset(&c, 0, sizeof c);
     c.gen_key = ~0ull;
+    c.mkey[0] = c.mkey[1] = c.mkey[2] = ~0ull;
     c.ticket = 0;
     c.t = 0;
     c.gf = INFINITY;
@@ -996,6 +997,7 @@ evox_status evox_pso_load(evox_pso* s, const void* host_blob, size_t size) {
     Ctl c;
     CU(s, cudaMemcpy(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost));
     c.gen_key = ~0ull;
+    c.mkey[0] = c.mkey[1] = c.mkey[2] = ~0ull;
     c.ticket = 0;
     c.t = h.t < 0 ? 0 : (unsigned long long)h.t;
     c.gf = h.gf;
@@ -1561,6 +1563,7 @@ evox_status evox_cso_load(evox_cso* s, const void* host_blob, size_t size) {
     Ctl c;
     CU(s, cudaMemcpy(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost));
     c.gen_key = ~0ull;
+    c.mkey[0] = c.mkey[1] = c.mkey[2] = ~0ull;
     c.ticket = 0;
     c.t = h.t < 0 ? 0 : (unsigned long long)h.t;
     CU(s, cudaMemcpy(s->ctl, &c, sizeof c, cudaMemcpyHostToDevice));
@@ -1954,6 +1957,7 @@ evox_status evox_de_load(evox_de* s, const void* host_blob, size_t size) {
     Ctl c;
     CU(s, cudaMemcpy(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost));
     c.gen_key = ~0ull;
+    c.mkey[0] = c.mkey[1] = c.mkey[2] = ~0ull;
     c.ticket = 0;
     c.t = h.t < 0 ? 0 : (unsigned long long)h.t;
     CU(s, cudaMemcpy(s->ctl, &c, sizeof c, cudaMemcpyHostToDevice));

@@ -29,6 +29,8 @@ struct Ctl {
     unsigned int fin_cnt;        // k_pso_fin: CTAs that staged their slice (reset by CTA 0)
     unsigned int fin_epoch;      // k_pso_fin: t_new + 1 once CTA 0 has decided the exchange
     int fin_sel;                 // k_pso_fin: rank whose staged row becomes gbest (-1: none)
+    unsigned int arrive;         // k_pso_run_mid (warp-row rows): monotonic arrival counter
+    unsigned long long mkey[3];  // its per-generation minimum keys, slot t % 3 (~0 at rest)
 };
 
 // One rank's PSO state, as seen by kernels.

@@ -716,6 +716,135 @@ __device__ __forceinline__ unsigned long long pso_tail_tile(const PsoArgs& a, lo
     return best;
 }
 
+#ifndef EVOX_MID_LOCAL_G
+#define EVOX_MID_LOCAL_G 1  // warp-row geometries: replicated gbest decision + CTA-local G copy
+#endif
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// The cooperative kernel's generations for warp-row geometries, without a "last CTA" on the
+// critical path: every CTA folds its minimum key into mkey[t % 3], arrives at a monotonic
+// counter and, once all have arrived, takes the SAME gbest decision from the same key and its
+// register copy of gf (strict improvement, R-5), and refreshes its own shared-memory copy of G
+// from the winner row (read through L2).  CTA 0 alone writes the host-visible state (G, gf,
+// gidx, hist, t) and resets the key slot of generation t + 2 (every CTA has read it: they all
+// passed this generation's barrier after reading it at the previous one).  Invariant between
+// launches: mkey[(t+1) % 3] and mkey[(t+2) % 3] are ~0.  Same decisions as pso_finalize: the
+// trajectory is bitwise the stepwise one.
+template <int P, class G, bool UNI>
+__device__ __forceinline__ void k_pso_run_mid_local(const PsoArgs& a, long long n, long long rw,
+                                                    int tr) {
+    __shared__ Fit<P> sh_acc[1];
+    __shared__ float sh_head[1];
+    __shared__ __align__(16) HStore<P, G> sh_h;
+    __shared__ unsigned char sh_pend[G::RPC];
+    __shared__ unsigned long long sh_k[WARPS];
+    __shared__ unsigned long long sh_key;
+    __shared__ int sh_abort;
+    extern __shared__ __align__(128) unsigned char mid_tail_smem[];  // [G copy][tail staging]
+    float* sG = reinterpret_cast<float*>(mid_tail_smem);
+    float4* tail_st = reinterpret_cast<float4*>(mid_tail_smem + ((a.ld * 4 + 127) / 128) * 128);
+    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+    const RowMap<G> m(a.ld >> 2);
+    Ctl* ctl = a.ctl;
+    for (long long j = threadIdx.x; j < a.ld; j += blockDim.x) sG[j] = a.G[j];
+    float gf = *(volatile float*)&ctl->gf;
+    // nobody arrives before every CTA has read the base: a whole generation comes first
+    const unsigned int base = *(volatile unsigned int*)&ctl->arrive;
+    unsigned long long t = *(volatile unsigned long long*)&ctl->t;
+    __syncthreads();
+    PsoArgs aw = a;  // rows [0, rw): the warps' whole rounds, G from shared memory
+    aw.rows = rw;
+    aw.G = sG;
+    PsoArgs at = a;  // rows [rw, rows): the tail tiles
+    at.G = sG;
+    const long long NQ = a.ld >> 2;
+    for (long long g = 0; g < n; ++g, ++t) {
+        unsigned long long best = pso_gen_rows<P, G, UNI, true>(aw, m, t, htab, sh_acc, sh_head);
+        if (tr > 0) {
+            const long long row0 = rw + (long long)blockIdx.x * tr;
+            const long long left = a.rows - row0;
+            const int nrow = left < tr ? (left > 0 ? (int)left : 0) : tr;
+            if (nrow > 0) {  // CTA-uniform
+                const unsigned long long k =
+                    pso_tail_tile<P, G, UNI>(at, row0, nrow, t, tail_st, htab, sh_acc, sh_head, sh_pend);
+                best = k < best ? k : best;
+            }
+        }
+#if EVOX_MID_PF
+        if (g + 1 < n && lane_id() == 0 && m.wfirst < a.rows) {
+            const long long nr = a.rows - m.wfirst < G::RPW ? a.rows - m.wfirst : G::RPW;
+            const long long o = m.wfirst * a.ld * 4;
+            long long bytes = nr * a.ld * 4;
+            if (bytes > 64 * 1024) bytes = 64 * 1024;
+            prefetch_l2(reinterpret_cast<const char*>(a.X) + o, bytes);
+            prefetch_l2(reinterpret_cast<const char*>(a.V) + o, bytes);
+            prefetch_l2(reinterpret_cast<const char*>(a.P) + o, bytes);
+        }
+#endif
+        // arrival: this CTA's rows visible device-wide, its minimum in the generation's slot
+        best = warp_min_u64(best);
+        if (lane_id() == 0) sh_k[threadIdx.x >> 5] = best;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long k = sh_k[0];
+#pragma unroll
+            for (int i = 1; i < WARPS; ++i) k = sh_k[i] < k ? sh_k[i] : k;
+            unsigned long long* slot = &ctl->mkey[t % 3];
+            if (k != ~0ull) atomicMin(slot, k);
+            __threadfence();
+            atomicAdd(&ctl->arrive, 1u);
+            const unsigned int target = base + (unsigned int)(g + 1) * gridDim.x;
+            int abort = 0;
+            const unsigned long long t0 = globaltimer_ns();
+            while ((int)(ld_acquire_gpu_u32(&ctl->arrive) - target) < 0) {
+                if (globaltimer_ns() - t0 > 10000000000ull) {  // 10 s: not co-resident
+                    ctl->err = 1;
+                    abort = 1;
+                    break;
+                }
+                __nanosleep(32);
+            }
+            sh_key = ld_acquire_gpu_u64(slot);
+            sh_abort = abort;
+        }
+        __syncthreads();
+        if (sh_abort) return;
+        // the replicated decision (pso_finalize's): strict improvement over gf
+        const unsigned long long key = sh_key;
+        const bool any = key != ~0ull;
+        const long long grow = (long long)(uint32_t)(key & 0xffffffffu);
+        const float fmin = any ? unord_f32((uint32_t)(key >> 32)) : __int_as_float(0x7f800000);
+        const bool better = any && fmin < gf;
+        if (better) {
+            const float4* src = reinterpret_cast<const float4*>(a.X + (grow - a.row0) * a.ld);
+            float4* dst = reinterpret_cast<float4*>(sG);
+            float4* Gg = reinterpret_cast<float4*>(a.G);
+            for (long long q = threadIdx.x; q < NQ; q += blockDim.x) {
+                const float4 v = __ldcg(src + q);
+                dst[q] = v;
+                if (blockIdx.x == 0) Gg[q] = v;
+            }
+            gf = fmin;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctl->mkey[(t + 2) % 3] = ~0ull;
+            if (better) {
+                ctl->gf = fmin;
+                ctl->gidx = grow;
+            }
+            ctl->hist[t + 1] = fmin;
+            ctl->t = t + 1;
+        }
+        __syncthreads();  // the shared G copy is complete
+    }
+}
+
 #ifndef EVOX_MID_U
 #define EVOX_MID_U 4     // chunks in flight of the cooperative kernel, warp-per-row geometry
 #endif
@@ -740,76 +869,80 @@ template <int P, class G, bool UNI>
 __global__ void __launch_bounds__(256, G::LPR == 4 ? EVOX_PSO_SHORT_MINB
                                                    : (G::WPR == 1 ? EVOX_MID_MINB : EVOX_MINB))
     k_pso_run_mid(PsoArgs a, long long n, long long rw, int tr) {
-    __shared__ Fit<P> sh_acc[G::WPR];
-    __shared__ float sh_head[G::WPR];
-    __shared__ __align__(16) HStore<P, G> sh_h;
-    __shared__ int sh_abort;
-    __shared__ unsigned char sh_pend[G::WPR == 1 ? G::RPC : 1];
-    extern __shared__ __align__(128) unsigned char mid_tail_smem[];  // tail staging (tr > 0)
-    const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
-    const RowMap<G> m(a.ld >> 2);
-    Ctl* ctl = a.ctl;
-    // nobody writes ctl->bar before every CTA has arrived at the first grid_argmin,
-    // so every CTA reads the same base
-    const unsigned int base = *(volatile unsigned int*)&ctl->bar;
-    unsigned long long t = *(volatile unsigned long long*)&ctl->t;
-    // rows [0, rw) are walked by the warps' whole rounds; with tr > 0, rows [rw, rows) are the
-    // tail tiles, tr rows per CTA (pso_tail_tile)
-    PsoArgs aw = a;
-    aw.rows = rw;
-    for (long long g = 0; g < n; ++g, ++t) {
-        unsigned long long best = pso_gen_rows<P, G, UNI, true>(aw, m, t, htab, sh_acc, sh_head);
-        if constexpr (G::WPR == 1) {
-            if (tr > 0) {
-                const long long row0 = rw + (long long)blockIdx.x * tr;
-                const long long left = a.rows - row0;
-                const int nrow = left < tr ? (left > 0 ? (int)left : 0) : tr;
-                if (nrow > 0) {  // CTA-uniform
-                    const unsigned long long k = pso_tail_tile<P, G, UNI>(
-                        a, row0, nrow, t, reinterpret_cast<float4*>(mid_tail_smem), htab, sh_acc,
-                        sh_head, sh_pend);
-                    best = k < best ? k : best;
-                }
-            }
-        }
-#if EVOX_MID_PF
-        // the warp's first rows of the next generation (its own, already final) go to L2
-        // while the grid drains the tail of this one (the pbest row only if not pending)
-        if (g + 1 < n && lane_id() == 0 && m.wfirst < a.rows) {
-            const long long nr = a.rows - m.wfirst < G::RPW ? a.rows - m.wfirst : G::RPW;
-            const long long o = m.wfirst * a.ld * 4 + m.qb * 16;
-            long long bytes = G::WPR == 1 ? nr * a.ld * 4 : (m.qe - m.qb) * 16;
-            if (bytes > 64 * 1024) bytes = 64 * 1024;
-            prefetch_l2(reinterpret_cast<const char*>(a.X) + o, bytes);
-            prefetch_l2(reinterpret_cast<const char*>(a.V) + o, bytes);
-            prefetch_l2(reinterpret_cast<const char*>(a.P) + o, bytes);
-        }
-#endif
-        unsigned long long key;
-        const unsigned int target = base + (unsigned int)g + 1u;
-        if (grid_argmin(ctl, best, &key)) {
-            pso_finalize(a, key, t + 1);  // G, gf, gidx, hist; gen_key/ticket reset; t
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                __threadfence();
-                st_release_gpu_u32(&ctl->bar, target);
-            }
-        } else if (g + 1 < n) {
-            if (threadIdx.x == 0) {
-                int abort = 0;
-                const unsigned long long t0 = globaltimer_ns();
-                while (ld_acquire_gpu_u32(&ctl->bar) != target) {
-                    if (globaltimer_ns() - t0 > 10000000000ull) {  // 10 s: not co-resident
-                        ctl->err = 1;
-                        abort = 1;
-                        break;
+    if constexpr (G::WPR == 1 && EVOX_MID_LOCAL_G) {
+        k_pso_run_mid_local<P, G, UNI>(a, n, rw, tr);
+    } else {
+        __shared__ Fit<P> sh_acc[G::WPR];
+        __shared__ float sh_head[G::WPR];
+        __shared__ __align__(16) HStore<P, G> sh_h;
+        __shared__ int sh_abort;
+        __shared__ unsigned char sh_pend[G::WPR == 1 ? G::RPC : 1];
+        extern __shared__ __align__(128) unsigned char mid_tail_smem[];  // tail staging (tr > 0)
+        const float* htab = HTable<P, G>::fill(sh_h.v, a.ld);
+        const RowMap<G> m(a.ld >> 2);
+        Ctl* ctl = a.ctl;
+        // nobody writes ctl->bar before every CTA has arrived at the first grid_argmin,
+        // so every CTA reads the same base
+        const unsigned int base = *(volatile unsigned int*)&ctl->bar;
+        unsigned long long t = *(volatile unsigned long long*)&ctl->t;
+        // rows [0, rw) are walked by the warps' whole rounds; with tr > 0, rows [rw, rows) are the
+        // tail tiles, tr rows per CTA (pso_tail_tile)
+        PsoArgs aw = a;
+        aw.rows = rw;
+        for (long long g = 0; g < n; ++g, ++t) {
+            unsigned long long best = pso_gen_rows<P, G, UNI, true>(aw, m, t, htab, sh_acc, sh_head);
+            if constexpr (G::WPR == 1) {
+                if (tr > 0) {
+                    const long long row0 = rw + (long long)blockIdx.x * tr;
+                    const long long left = a.rows - row0;
+                    const int nrow = left < tr ? (left > 0 ? (int)left : 0) : tr;
+                    if (nrow > 0) {  // CTA-uniform
+                        const unsigned long long k = pso_tail_tile<P, G, UNI>(
+                            a, row0, nrow, t, reinterpret_cast<float4*>(mid_tail_smem), htab, sh_acc,
+                            sh_head, sh_pend);
+                        best = k < best ? k : best;
                     }
-                    __nanosleep(64);
                 }
-                sh_abort = abort;
             }
-            __syncthreads();
-            if (sh_abort) return;
+    #if EVOX_MID_PF
+            // the warp's first rows of the next generation (its own, already final) go to L2
+            // while the grid drains the tail of this one (the pbest row only if not pending)
+            if (g + 1 < n && lane_id() == 0 && m.wfirst < a.rows) {
+                const long long nr = a.rows - m.wfirst < G::RPW ? a.rows - m.wfirst : G::RPW;
+                const long long o = m.wfirst * a.ld * 4 + m.qb * 16;
+                long long bytes = G::WPR == 1 ? nr * a.ld * 4 : (m.qe - m.qb) * 16;
+                if (bytes > 64 * 1024) bytes = 64 * 1024;
+                prefetch_l2(reinterpret_cast<const char*>(a.X) + o, bytes);
+                prefetch_l2(reinterpret_cast<const char*>(a.V) + o, bytes);
+                prefetch_l2(reinterpret_cast<const char*>(a.P) + o, bytes);
+            }
+    #endif
+            unsigned long long key;
+            const unsigned int target = base + (unsigned int)g + 1u;
+            if (grid_argmin(ctl, best, &key)) {
+                pso_finalize(a, key, t + 1);  // G, gf, gidx, hist; gen_key/ticket reset; t
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    st_release_gpu_u32(&ctl->bar, target);
+                }
+            } else if (g + 1 < n) {
+                if (threadIdx.x == 0) {
+                    int abort = 0;
+                    const unsigned long long t0 = globaltimer_ns();
+                    while (ld_acquire_gpu_u32(&ctl->bar) != target) {
+                        if (globaltimer_ns() - t0 > 10000000000ull) {  // 10 s: not co-resident
+                            ctl->err = 1;
+                            abort = 1;
+                            break;
+                        }
+                        __nanosleep(64);
+                    }
+                    sh_abort = abort;
+                }
+                __syncthreads();
+                if (sh_abort) return;
+            }
         }
     }
 }
@@ -1331,10 +1464,21 @@ cudaError_t launch_pso_run_mid(int problem, const PsoArgs& a, long long n, cudaS
         const void* fn = (const void*)k_pso_run_mid<P_, GM_, U_>;
         // the tail split: the rows beyond the grid's whole rounds as flat tiles of <= tr rows
         // per CTA, when their staging fits EVOX_MID_TAIL bytes (warp-row geometries)
-        size_t smem = 0;
+        const size_t gcopy = (GM_::WPR == 1 && EVOX_MID_LOCAL_G) ? (size_t)((a.ld * 4 + 127) / 128) * 128 : 0;
+        size_t smem = gcopy;
         long long rw = a.rows;
         int tr = 0;
-        int grid = grid_for(fn, row_units<G_>(a.rows), dev);  // resident grid only
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + 32768));
+        int grid = 1;
+        {
+            int per_sm = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+            if (per_sm < 1) per_sm = 1;
+            long long g = (long long)sm_count(dev) * per_sm;  // resident grid only
+            const long long units = row_units<G_>(a.rows);
+            grid = (int)(units < g ? units : g);
+        }
         if (GM_::WPR == 1 && EVOX_MID_TAIL > 0) {
             const long long slots = (long long)grid * GM_::RPC;  // rows per round of the grid
             const long long full = a.rows / slots * slots;
@@ -1343,11 +1487,11 @@ cudaError_t launch_pso_run_mid(int problem, const PsoArgs& a, long long n, cudaS
             const size_t bytes = (size_t)t_r * (size_t)a.ld * 4 * stage_comps<P_>();
             if (tail > 0 && t_r <= GM_::RPC && bytes <= (size_t)EVOX_MID_TAIL) {
                 int per_sm = 1;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, bytes);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, gcopy + bytes);
                 if ((long long)per_sm * sm_count(dev) >= grid) {  // still co-resident
                     rw = full;
                     tr = (int)t_r;
-                    smem = bytes;
+                    smem = gcopy + bytes;
                 }
             }
         }
