@@ -716,6 +716,9 @@ __device__ __forceinline__ unsigned long long pso_tail_tile(const PsoArgs& a, lo
     return best;
 }
 
+#ifndef EVOX_MID_ALL_FENCE
+#define EVOX_MID_ALL_FENCE 0  // every thread fences before the arrival (measurement knob)
+#endif
 #ifndef EVOX_MID_LOCAL_G
 #define EVOX_MID_LOCAL_G 1  // warp-row geometries: replicated gbest decision + CTA-local G copy
 #endif
@@ -786,10 +789,13 @@ __device__ __forceinline__ void k_pso_run_mid_local(const PsoArgs& a, long long 
             prefetch_l2(reinterpret_cast<const char*>(a.P) + o, bytes);
         }
 #endif
-        // arrival: this CTA's rows visible device-wide, its minimum in the generation's slot
+        // arrival: this CTA's rows visible device-wide (bar.sync, then thread 0's cumulative
+        // fence -- the grid-sync pattern), its minimum in the generation's slot
         best = warp_min_u64(best);
         if (lane_id() == 0) sh_k[threadIdx.x >> 5] = best;
+#if EVOX_MID_ALL_FENCE
         __threadfence();
+#endif
         __syncthreads();
         if (threadIdx.x == 0) {
             unsigned long long k = sh_k[0];
