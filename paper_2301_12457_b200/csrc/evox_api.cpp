@@ -519,6 +519,10 @@ struct evox_pso : Base {
     std::vector<void*> ipc_opened;
     bool asked = false;   // ask issued, tell pending
     int64_t ask_t = 0;    // population index the pending tell refers to
+    // t right after the last cooperative launch: its per-generation key slots (Ctl::mkey) are
+    // clean for a launch starting there; any other t (another path advanced the population,
+    // or a load) re-initialises them first
+    int64_t mid_t = -2;
     PsoArgs args() const {
         PsoArgs a;
         std::memset(&a, 0, sizeof a);
@@ -773,9 +777,12 @@ evox_status evox_pso_step(evox_pso* s, evox_problem problem, int64_t n_gens) {
     // EVOX_FLAG_NO_MID: per-generation launches at every size (testing / A-B timing)
     const bool no_mid = (s->flags & EVOX_FLAG_NO_MID) != 0;
     if (!s->comm && !s->peer && !no_mid && !no_small && evox::pso_mid(s->rows, s->ld)) {
+        if (s->mid_t != s->t)
+            CU(s, cudaMemsetAsync(&s->ctl->mkey, 0xff, sizeof(s->ctl->mkey), s->stream));
         CU(s, timed(s, [&] { return evox::launch_pso_run_mid((int)problem, a, n_gens, s->stream); },
                     n_gens));
         s->t += n_gens;
+        s->mid_t = s->t;
         return EVOX_OK;
     }
     st = run_graphed(s, (int)problem, n_gens, [&]() -> evox_status {
@@ -1004,6 +1011,7 @@ evox_status evox_pso_load(evox_pso* s, const void* host_blob, size_t size) {
     c.gidx = h.gidx;
     CU(s, cudaMemcpy(s->ctl, &c, sizeof c, cudaMemcpyHostToDevice));
     s->t = h.t;
+    s->mid_t = -2;
     s->problem = (int)h.problem;
     s->asked = h.asked != 0;
     s->ask_t = h.ask_t;

@@ -203,6 +203,30 @@ def test_pso_mid_kernel_equals_stepwise(problem, N, D):
     assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
 
 
+def test_pso_mid_kernel_interleaved_with_ask_tell():
+    """Cooperative launches interleaved with unfused ask/tell generations (other paths advancing
+    the population between launches, so the cooperative kernel's per-generation key slots must be
+    re-initialised) -- bitwise the same generations all run one launch at a time."""
+    N, D, p = 3001, 1000, "ackley"
+    lb, ub = WL.BOUNDS[p]
+    a = ev.PSO(N, D, lb, ub, seed=19)
+    b = ev.PSO(N, D, lb, ub, seed=19, flags=E.FLAG_NO_MID)
+    def ask_tell(h):  # evaluated on the handle's stream, so it sees ask's population
+        h.tell(ev.evaluate(p, h.ask(), dim=D, stream=h.stream))
+
+    for h in (a, b):
+        h.step(p, 3)
+        for _ in range(2):  # two unfused generations
+            ask_tell(h)
+        h.step(p, 4)
+        ask_tell(h)
+        h.step(p, 2)
+    ga, gb = gpu_pso_state(a, D), gpu_pso_state(b, D)
+    for k in ("X", "V", "P", "f", "pf", "G", "hist"):
+        assert np.array_equal(ga[k], gb[k]), k
+    assert ga["gidx"] == gb["gidx"] and ga["gf"] == gb["gf"]
+
+
 @pytest.mark.parametrize("problem,N,D", [("ackley", 3001, 1000), ("rosenbrock", 3001, 100),
                                          ("rastrigin", 700, 1001), ("griewank", 3001, 1000),
                                          ("sphere", 2401, 257)])
