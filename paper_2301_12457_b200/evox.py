@@ -402,7 +402,9 @@ class PSO(_Handle):
         _check(lib().evox_pso_step(self._h, problem_id(problem), int(n_gens)))
 
     def ask(self):
-        """Algorithm.ask: borrowed [rows, ld] view of the population to evaluate."""
+        """Algorithm.ask: borrowed [rows, ld] view of the population to evaluate.  The move
+        that produces it is queued on `self.stream`: evaluate it on that stream (e.g.
+        `evaluate(problem, X, stream=pso.stream)`) or synchronize first."""
         ptr, rows, ld = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int64()
         _check(lib().evox_pso_ask(self._h, ctypes.byref(ptr), ctypes.byref(rows),
                                   ctypes.byref(ld)))

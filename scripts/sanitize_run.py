@@ -14,7 +14,7 @@ for D in (10, 100, 1003, 4099):
         pso = ev.PSO(37, D, -5, 5, seed=1)
         pso.step(p, 3)
         X = pso.ask()
-        pso.tell(ev.evaluate(p, X.clone(), dim=D, stream=pso.stream))
+        pso.tell(ev.evaluate(p, X, dim=D, stream=pso.stream))  # on the handle's stream
         pso.view("P")
         pso.best()
         cso = ev.CSO(40, D, -5, 5, block=10, seed=1)
