@@ -716,6 +716,9 @@ __device__ __forceinline__ unsigned long long pso_tail_tile(const PsoArgs& a, lo
     return best;
 }
 
+#ifndef EVOX_MID_SPIN_NS
+#define EVOX_MID_SPIN_NS 32  // back-off of the arrival spin (measurement knob)
+#endif
 #ifndef EVOX_MID_ALL_FENCE
 #define EVOX_MID_ALL_FENCE 0  // every thread fences before the arrival (measurement knob)
 #endif
@@ -814,7 +817,7 @@ __device__ __forceinline__ void k_pso_run_mid_local(const PsoArgs& a, long long 
                     abort = 1;
                     break;
                 }
-                __nanosleep(32);
+                if (EVOX_MID_SPIN_NS > 0) __nanosleep(EVOX_MID_SPIN_NS);
             }
             sh_key = ld_acquire_gpu_u64(slot);
             sh_abort = abort;
